@@ -1,0 +1,83 @@
+/*
+ * efta_b200.h — C-ABI of the B200-native EFTA hot path (libefta_b200.so).
+ *
+ * Plain pointers and sizes only (no CUDA / torch types): `stream` is a
+ * cudaStream_t passed as void*. Unless stated otherwise every data pointer is
+ * a DEVICE pointer owned by the caller; nothing is allocated on the hot path.
+ * Return codes: 0 ok, 1 configuration error (the reference's ConfigError),
+ * 2 CUDA error; efta_last_error() describes the last failure (thread-local).
+ *
+ * Each entry point replaces a reference interface (paths relative to
+ * /root/reference/proj):
+ *
+ *   efta_attn_fwd_f16        efta::efta_forward            include/efta/efta.hpp:86-89
+ *                            (modes NONE / EFTA / EFTA_OPTIMIZED; the FaultInjector*
+ *                            argument becomes the device fault table; FTReport
+ *                            becomes events + counters + m/l outputs)
+ *   efta_attn_validate       efta::AttnConfig::validate    include/efta/config.hpp:30-41
+ *   efta_attn_fwd_host_f16   same as efta_attn_fwd_f16, HOST buffers in/out (copies
+ *                            inside the call: the reference-facing e2e path)
+ *   efta_abft_gemm_f16       efta::checksummed_gemm + verify_locate_correct
+ *                            include/efta/abft.hpp:58-60, 73-77 (strided-ABFT GEMM,
+ *                            applied per 256-wide output column tile = FFN linear)
+ *   efta_abft_encode_weight_f16  encode_strided of a weight matrix, abft.hpp:38
+ *   efta_flip_bit            efta::flip_bit                 include/efta/fault.hpp:33
+ */
+#ifndef EFTA_B200_H
+#define EFTA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../paper_2504_02211_b200/csrc/efta_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Attention problem: Q, K, V are [batch*heads, seq_len, head_dim] fp16 (bits as
+ * uint16), O is fp32 of the same shape, m_out / l_out are [batch*heads, seq_len]
+ * fp32 (the reference's FTReport::final_m / final_l). */
+typedef struct {
+    int batch, heads, seq_len, head_dim;
+    int block;          /* reference AttnConfig::block; this kernel: 128 */
+    int stride;         /* reference AttnConfig::stride; this kernel: 8 */
+    float scale;        /* 0 -> 1/sqrt(head_dim) (config.hpp:40) */
+    int mode;           /* efta_mode */
+    double eps1, eps2, eps_lin; /* reference Thresholds (snvr.hpp:17-30) */
+    int observe_linear; /* KernelKnobs::observe_linear (efta.hpp:79) */
+    float rowmax_bias;  /* KernelKnobs::rowmax_bias (efta.hpp:82) */
+    int debug;          /* 1: fault-tap / observation kernel variant (required if n_faults > 0) */
+} efta_attn_desc;
+
+const char* efta_last_error(void);
+int efta_attn_validate(const efta_attn_desc* d);
+size_t efta_attn_workspace_bytes(const efta_attn_desc* d);
+
+/* counters: device efta_counters (zeroed by the call). events/fired: device arrays
+ * of the given capacities (may be NULL with cap 0). faults: device array. */
+int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t* k,
+                      const uint16_t* v, float* o, float* m_out, float* l_out, void* workspace,
+                      size_t workspace_bytes, const efta_fault_spec* faults, int n_faults,
+                      efta_event* events, int ev_cap, efta_fired* fired, int fired_cap,
+                      efta_counters* counters, void* stream);
+
+/* Same contract with HOST buffers (q/k/v/o/m/l/faults/events/fired/counters all
+ * host memory); device scratch is cached per thread and reused across calls.
+ * Synchronous. */
+int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t* k,
+                           const uint16_t* v, float* o, float* m_out, float* l_out,
+                           const efta_fault_spec* faults, int n_faults, efta_event* events,
+                           int ev_cap, efta_fired* fired, int fired_cap, efta_counters* counters);
+
+/* Strided checksum operands of K and V only (the encode prepass the forward runs
+ * internally); kc: [BH*nblk*32, head_dim] fp16, vc: [BH*nblk*32, 128] fp16. */
+int efta_attn_encode_kv_f16(const efta_attn_desc* d, const uint16_t* k, const uint16_t* v,
+                            uint16_t* kc, uint16_t* vc, void* stream);
+
+float efta_flip_bit(float v, int width, int bit);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

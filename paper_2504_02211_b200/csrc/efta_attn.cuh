@@ -1,0 +1,328 @@
+// efta_attn.cuh — fused end-to-end fault-tolerant attention forward for sm_100a.
+//
+// Replaces the reference's efta_forward (src/efta.cpp:72-351) for one
+// [batch*heads, seq, d] fp16 problem. One CTA owns one (head, 128-row query
+// block) = the reference's row-block i; it streams the key/value blocks j
+// (B_c = 128) with the reference's online-softmax recurrence (rescale every
+// iteration, src/efta.cpp:192-260).
+//
+// Warp roles (256 threads):
+//   warp 0      TMA producer for K_j (+ its strided checksum rows KC_j)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warp 3      TMA producer for V_j (+ VC_j) and Q
+//   warps 4..7  "row warpgroup": thread t owns query row t == TMEM lane t.
+//               Softmax, exp-stage check, factor guard, O rescale (correction),
+//               epilogue normalisation + final output check + store.
+//
+// TMEM columns (512 allocated):
+//   S[b]   = b*128     (b = j&1; P_j (fp16x2) is written over its first 64 cols)
+//   Scs[b] = 256+16b   (16 cols: c1[0..7] c2[0..7] of S = Q.[KC_hi;KC_lo]^T)
+//   O      = 288       (D cols), Ocs = 288+D (16 cols: strided checksums of O)
+//
+// Checksum operands (hi/lo fp16 split of the fp32 strided sums, produced by
+// efta_encode_kv in efta_encode.cu) ride alongside every K/V tile:
+//   KC_j  [32 x D]   rows 0-7 c1_hi, 8-15 c2_hi, 16-23 c1_lo, 24-31 c2_lo
+//   VC_j  [32 x 128] same row order, columns = keys of the block
+// so S's checksum columns come out of the same tcgen05 pipe as S (two N=16
+// MMAs accumulating hi then lo) and O's checksum columns out of the PV MMAs.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include <math_constants.h>
+
+#include "efta_types.h"
+#include "sm100_ptx.cuh"
+
+namespace efta_sm100 {
+
+constexpr int kBlock = 128;   // B_r = B_c (reference AttnConfig::block)
+constexpr int kStride = 8;    // s   (reference AttnConfig::stride)
+constexpr int kCsCols = 2 * kStride;  // c1 | c2
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct AttnParams {
+    int seq_len, nblk, n_heads_flat;
+    float scale, scale_log2, rowmax_bias;
+    double eps1, eps2, eps_lin;
+    float* o;        // [BH, S, D] fp32
+    float* m_out;    // [BH, S]
+    float* l_out;    // [BH, S]
+    efta_event* events;
+    int ev_cap;
+    efta_counters* counters;
+    const efta_fault_spec* faults;
+    int n_faults;
+    efta_fired* fired;
+    int fired_cap;
+    int observe_linear;
+};
+
+template <int D>
+struct AttnLayout {
+    static constexpr int NSUB = D / 64;
+    static constexpr int KS = (D == 64) ? 3 : 2;  // K ring stages
+    static constexpr int VS = (D == 64) ? 3 : 2;  // V ring stages
+    static constexpr uint32_t Q_BYTES = NSUB * 16384;
+    static constexpr uint32_t K_BYTES = NSUB * 16384;
+    static constexpr uint32_t KC_BYTES = NSUB * 4096;
+    static constexpr uint32_t V_BYTES = NSUB * 16384;
+    static constexpr uint32_t VC_BYTES = 2 * 4096;
+    static constexpr uint32_t K_STAGE = K_BYTES + KC_BYTES;
+    static constexpr uint32_t V_STAGE = V_BYTES + VC_BYTES;
+    static constexpr uint32_t OFF_Q = 0;
+    static constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
+    static constexpr uint32_t OFF_V = OFF_K + KS * K_STAGE;
+    static constexpr uint32_t OFF_BAR = OFF_V + VS * V_STAGE;
+    // barriers: q_full, k_full[KS], k_empty[KS], v_full[VS], v_empty[VS], s_full[2],
+    //           p_ready, o_done  -> then tmem slot + scratch for tile reductions
+    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2;
+    static constexpr uint32_t OFF_TMEM = OFF_BAR + NBAR * 8;
+    static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
+    static constexpr uint32_t RED_BYTES = 128 * 24 + 256;  // RowSlot[128] + ints + doubles
+    static constexpr uint32_t SMEM_BYTES = OFF_RED + RED_BYTES + 1024;  // + alignment slack
+    static constexpr uint32_t COL_S0 = 0, COL_SCS0 = 256, COL_O = 288, COL_OCS = 288 + D;
+    static constexpr uint32_t TMEM_COLS = 512;
+};
+
+// ---------------------------------------------------------------- fault taps
+// Per-thread injector state. The reference allows at most one spec per
+// row-block (src/fault.cpp:117-119), so a (head, block_i) CTA has <= 1 spec
+// and only the thread owning spec.row evaluates it. Evaluation counting and
+// trigger semantics mirror FaultInjector::tap (include/efta/fault.hpp:82-95).
+struct ThreadTap {
+    int active, site, bj, col, bit, trigger, count, idx;
+    __device__ __forceinline__ float operator()(const AttnParams& p, int s, int j, int c,
+                                                float v) {
+        if (!active || s != site || j != bj || c != col) return v;
+        if (++count != trigger) return v;
+        const float flipped = __uint_as_float(__float_as_uint(v) ^ (1u << bit));
+        const int slot = atomicAdd(&p.counters->n_fired, 1);
+        if (slot < p.fired_cap) {
+            p.fired[slot].spec = p.faults[idx];
+            p.fired[slot].before = v;
+            p.fired[slot].after = flipped;
+        }
+        return flipped;
+    }
+};
+
+__device__ __forceinline__ void atomic_max_nonneg(float* addr, float v) {
+    if (!(v >= 0.0f)) return;
+    if (isinf(v)) return;  // the reference's calibration ignores non-finite residuals
+    atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
+}
+
+__device__ __forceinline__ void push_event(const AttnParams& p, int kind, int head, int bi,
+                                           int bj, int status, int row, int col, int violations,
+                                           int corrections, int checksum_repair, double residual,
+                                           double delta) {
+    // reference FTReport::push_event (src/efta.cpp:49-55): only non-CLEAN
+    // events are logged on the device; detections / corrections / failed
+    // aggregate exactly like the reference's counters.
+    efta_counters* c = p.counters;
+    if (status != EFTA_CLEAN) atomicAdd(&c->detections, 1);
+    if (corrections) atomicAdd(&c->corrections, corrections);
+    if (status == EFTA_DETECTED_UNCORRECTABLE || status == EFTA_NONFINITE) atomicExch(&c->failed, 1);
+    if (status == EFTA_CLEAN) return;
+    const int slot = atomicAdd(&c->n_events, 1);
+    if (slot >= p.ev_cap) return;
+    efta_event& e = p.events[slot];
+    e.kind = kind;
+    e.head = head;
+    e.block_i = bi;
+    e.block_j = bj;
+    e.status = status;
+    e.row = row;
+    e.col = col;
+    e.violations = violations;
+    e.corrections = corrections;
+    e.checksum_repair = checksum_repair;
+    e.residual = residual;
+    e.delta = delta;
+}
+
+// ------------------------------------------------- strided verify of one row
+// Row-local restatement of verify_locate_correct (src/abft.cpp:65-187) for
+// the G = W/8 groups of one thread-owned row (no shuffles: the whole row and
+// its 2x8 checksums live in this thread). Operates on a local array (only used
+// on the slow path). The caller handles the tile-wide "checksum non-finite"
+// early return (abft.cpp:74-78).
+struct RowVerify {
+    int violations, corrections, checksum_repair, uncorrectable, nonfinite;
+    int restored_col;      // last erasure-restored column (-1 none)
+    double residual;
+    double best_abs;       // largest |applied| correction (strict >, first wins)
+    double best_delta;     // signed value of that correction
+    int best_col;
+};
+
+template <int W>
+__device__ __noinline__ void verify_row(float* t, const float* c1, const float* c2, double eps_row,
+                                        RowVerify& rv) {
+    constexpr int G = W / kStride;
+    rv.violations = rv.corrections = rv.checksum_repair = rv.uncorrectable = rv.nonfinite = 0;
+    rv.restored_col = -1;
+    rv.residual = 0.0;
+    rv.best_abs = 0.0;
+    rv.best_delta = 0.0;
+    rv.best_col = -1;
+    bool any_nonfinite = false;
+    for (int c = 0; c < W; ++c) any_nonfinite |= !isfinite(t[c]);
+    if (any_nonfinite) {  // abft.cpp:83-111 erasure restore
+        for (int j = 0; j < kStride; ++j) {
+            int bad = -1, bad_count = 0;
+            for (int l = 0; l < G; ++l)
+                if (!isfinite(t[j + kStride * l])) { bad = l; ++bad_count; }
+            if (bad_count == 0) continue;
+            ++rv.violations;
+            if (bad_count > 1) { rv.nonfinite = 1; rv.residual = CUDART_INF; return; }
+            float rest = 0.0f;
+            for (int l = 0; l < G; ++l)
+                if (l != bad) rest = __fadd_rn(rest, t[j + kStride * l]);
+            const int col = j + kStride * bad;
+            t[col] = __fsub_rn(c1[j], rest);
+            ++rv.corrections;
+            rv.restored_col = col;
+        }
+    }
+    for (int j = 0; j < kStride; ++j) {
+        float a = 0.0f, b = 0.0f;
+        for (int l = 0; l < G; ++l) {
+            const float v = t[j + kStride * l];
+            a = __fadd_rn(a, v);
+            b = __fadd_rn(b, __fmul_rn(static_cast<float>(l + 1), v));
+        }
+        double s1d = a, s2d = b;
+        if (!isfinite(s1d) || !isfinite(s2d)) {  // abft.cpp:120-131
+            s1d = 0.0;
+            s2d = 0.0;
+            for (int l = 0; l < G; ++l) {
+                const double vv = t[j + kStride * l];
+                s1d += vv;
+                s2d += (l + 1.0) * vv;
+            }
+        }
+        const double d1 = static_cast<double>(c1[j]) - s1d;
+        const double d2 = static_cast<double>(c2[j]) - s2d;
+        rv.residual = fmax(rv.residual, fmax(fabs(d1), fabs(d2) / G));
+        const bool v1 = fabs(d1) > eps_row;
+        const bool v2 = fabs(d2) > eps_row * G;
+        if (!v1 && !v2) continue;
+        ++rv.violations;
+        if (!v1) { rv.checksum_repair = 1; continue; }
+        const double ratio = d2 / d1;
+        const double nearest = round(ratio);
+        if (nearest == 0.0 && fabs(ratio) <= 0.25) { rv.checksum_repair = 1; continue; }
+        const int g = static_cast<int>(nearest) - 1;
+        if (g < 0 || g >= G || fabs(ratio - nearest) > 0.25) {
+            if (fmax(fabs(d1), fabs(d2) / G) > eps_row * 16.0) rv.uncorrectable = 1;
+            continue;
+        }
+        const int col = j + kStride * g;
+        float rest = 0.0f;
+        for (int l = 0; l < G; ++l)
+            if (l != g) rest = __fadd_rn(rest, t[j + kStride * l]);
+        const float old_val = t[col];
+        const float new_val = __fsub_rn(c1[j], rest);
+        t[col] = new_val;
+        ++rv.corrections;
+        const double applied = static_cast<double>(new_val) - static_cast<double>(old_val);
+        if (fabs(applied) > rv.best_abs) {
+            rv.best_abs = fabs(applied);
+            rv.best_delta = applied;
+            rv.best_col = col;
+        }
+    }
+}
+
+// Tile-level aggregation of per-row RowVerify records into one reference
+// VerificationReport (rows visited in order, abft.cpp:116-186). `red` is
+// shared scratch: 128 x {best_abs(double), best_col, restored_col}.
+struct TileReport {
+    int status, row, col, violations, corrections, checksum_repair;
+    double residual, delta;
+};
+
+struct RowSlot {
+    double best_abs, best_delta;
+    int best_col, restored_col;
+};
+
+__device__ __forceinline__ void wg_sync() { named_bar_sync(1, 128); }
+
+// All 128 row threads call this; returns the tile report on thread 0 (row 0).
+static __device__ __noinline__ TileReport reduce_tile_report(const RowVerify& rv, bool tile_nonfinite,
+                                                     int row, RowSlot* slots, int* ints,
+                                                     double* dbl) {
+    // ints: [0] violations [1] corrections [2] checksum_repair [3] uncorrectable [4] nonfinite
+    if (row == 0) {
+        for (int i = 0; i < 5; ++i) ints[i] = 0;
+        dbl[0] = 0.0;
+    }
+    wg_sync();
+    atomicAdd(&ints[0], rv.violations);
+    atomicAdd(&ints[1], rv.corrections);
+    if (rv.checksum_repair) atomicOr(&ints[2], 1);
+    if (rv.uncorrectable) atomicOr(&ints[3], 1);
+    if (rv.nonfinite) atomicOr(&ints[4], 1);
+    slots[row].best_abs = rv.best_abs;
+    slots[row].best_delta = rv.best_delta;
+    slots[row].best_col = rv.best_col;
+    slots[row].restored_col = rv.restored_col;
+    // residual max through a CAS loop on doubles (rare path)
+    {
+        unsigned long long* a = reinterpret_cast<unsigned long long*>(&dbl[0]);
+        unsigned long long old = *a, assumed;
+        do {
+            assumed = old;
+            if (__longlong_as_double(assumed) >= rv.residual || isnan(rv.residual)) break;
+            old = atomicCAS(a, assumed, __double_as_longlong(rv.residual));
+        } while (old != assumed);
+    }
+    wg_sync();
+    TileReport tr{};
+    if (row == 0) {
+        tr.violations = ints[0];
+        tr.corrections = ints[1];
+        tr.checksum_repair = ints[2];
+        tr.residual = dbl[0];
+        tr.row = -1;
+        tr.col = -1;
+        tr.delta = 0.0;
+        if (tile_nonfinite || ints[4]) {
+            tr.status = EFTA_NONFINITE;
+            tr.residual = CUDART_INF;
+        } else {
+            double best = 0.0, best_signed = 0.0;
+            int last_restored_row = -1, last_restored_col = -1;
+            for (int r = 0; r < 128; ++r) {
+                if (slots[r].restored_col >= 0) {
+                    last_restored_row = r;
+                    last_restored_col = slots[r].restored_col;
+                }
+                if (slots[r].best_col >= 0 && slots[r].best_abs > best) {
+                    best = slots[r].best_abs;
+                    best_signed = slots[r].best_delta;
+                    tr.row = r;
+                    tr.col = slots[r].best_col;
+                }
+            }
+            if (last_restored_row >= 0) {  // erasure restore sets delta = inf (abft.cpp:105-107)
+                tr.row = last_restored_row;
+                tr.col = last_restored_col;
+                tr.delta = CUDART_INF;
+            } else {
+                tr.delta = best_signed;
+            }
+            if (ints[3]) tr.status = EFTA_DETECTED_UNCORRECTABLE;
+            else if (tr.corrections > 0 || tr.checksum_repair) tr.status = EFTA_CORRECTED;
+            else tr.status = EFTA_CLEAN;
+        }
+    }
+    wg_sync();
+    return tr;
+}
+
+}  // namespace efta_sm100

@@ -1,0 +1,62 @@
+// efta_attn_inst.cu — instantiations of the fused attention kernel for one head
+// dim (EFTA_INST_D), all modes x {fast, debug/tap} variants.
+#include "efta_attn_kernel.cuh"
+#include "efta_launch.h"
+
+#ifndef EFTA_INST_D
+#error "EFTA_INST_D must be 64 or 128"
+#endif
+
+using namespace efta_sm100;
+
+namespace {
+
+template <int D, int MODE, bool DBG>
+cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                     const CUtensorMap& tkc, const CUtensorMap& tvc, const AttnParams& p, int bh,
+                     cudaStream_t st) {
+    using L = AttnLayout<D>;
+    auto kern = efta_attn_fwd_kernel<D, MODE, DBG>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             L::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    dim3 grid(p.nblk, bh);
+    kern<<<grid, 256, L::SMEM_BYTES, st>>>(tq, tk, tv, tkc, tvc, p);
+    return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_d(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMap& tk,
+                     const CUtensorMap& tv, const CUtensorMap& tkc, const CUtensorMap& tvc,
+                     const AttnParams& p, int bh, cudaStream_t st) {
+    switch (mode * 2 + (dbg ? 1 : 0)) {
+        case 0: return launch_t<D, 0, false>(tq, tk, tv, tkc, tvc, p, bh, st);
+        case 1: return launch_t<D, 0, true>(tq, tk, tv, tkc, tvc, p, bh, st);
+        case 2: return launch_t<D, 1, false>(tq, tk, tv, tkc, tvc, p, bh, st);
+        case 3: return launch_t<D, 1, true>(tq, tk, tv, tkc, tvc, p, bh, st);
+        case 4: return launch_t<D, 2, false>(tq, tk, tv, tkc, tvc, p, bh, st);
+        default: return launch_t<D, 2, true>(tq, tk, tv, tkc, tvc, p, bh, st);
+    }
+}
+
+}  // namespace
+
+#if EFTA_INST_D == 64
+cudaError_t efta_launch_attn_d64(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMap& tk,
+                                 const CUtensorMap& tv, const CUtensorMap& tkc,
+                                 const CUtensorMap& tvc, const AttnParams& p, int bh,
+                                 cudaStream_t st) {
+    return launch_d<64>(mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
+}
+#else
+cudaError_t efta_launch_attn_d128(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMap& tk,
+                                  const CUtensorMap& tv, const CUtensorMap& tkc,
+                                  const CUtensorMap& tvc, const AttnParams& p, int bh,
+                                  cudaStream_t st) {
+    return launch_d<128>(mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
+}
+#endif

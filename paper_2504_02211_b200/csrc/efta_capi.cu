@@ -1,0 +1,267 @@
+// efta_capi.cu — C-ABI entry points (include/efta_b200.h): validation, TMA
+// descriptor construction, kernel dispatch. No torch, no CPU fallback: every
+// compute entry point launches sm_100a kernels or fails with a CUDA error.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/efta_b200.h"
+#include "efta_attn.cuh"
+#include "efta_launch.h"
+#include "efta_encode.cuh"
+
+using namespace efta_sm100;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(2, std::string(#expr) + ": " + cudaGetErrorString(e_));              \
+    } while (0)
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 2D fp16 tensor [rows, cols] row-major, box {64, box_rows}, 128B swizzle.
+bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int validate(const efta_attn_desc* d) {
+    if (!d) return fail(1, "efta: null descriptor");
+    // reference AttnConfig::validate (include/efta/config.hpp:30-41)
+    if (d->seq_len <= 0 || d->head_dim <= 0 || d->block <= 0 || d->stride <= 0 || d->heads <= 0 ||
+        d->batch <= 0)
+        return fail(1, "config: dimensions must be positive");
+    if (d->seq_len % d->block != 0)
+        return fail(1, "config: block must divide seq_len (" + std::to_string(d->block) + " vs " +
+                           std::to_string(d->seq_len) + ")");
+    if (d->block % d->stride != 0) return fail(1, "config: stride must divide block");
+    if (d->head_dim % d->stride != 0) return fail(1, "config: stride must divide head_dim");
+    // geometry of this sm_100a kernel
+    if (d->block != kBlock) return fail(1, "efta_b200: block must be 128 (tcgen05 M=128 tile)");
+    if (d->stride != kStride) return fail(1, "efta_b200: stride must be 8");
+    if (d->head_dim != 64 && d->head_dim != 128) return fail(1, "efta_b200: head_dim must be 64 or 128");
+    if (d->mode < EFTA_MODE_NONE || d->mode > EFTA_MODE_EFTA_OPT)
+        return fail(1, "efta_b200: unsupported mode (DECOUPLED is not provided)");
+    const long long bh = static_cast<long long>(d->batch) * d->heads;
+    if (bh > 65535) return fail(1, "efta_b200: batch*heads must be <= 65535");
+    return 0;
+}
+
+size_t ws_bytes(const efta_attn_desc* d) {
+    const size_t bh = static_cast<size_t>(d->batch) * d->heads;
+    const size_t nblk = d->seq_len / kBlock;
+    return bh * nblk * 32 * (d->head_dim + 128) * sizeof(__half) + 256;
+}
+
+int encode_kv(const efta_attn_desc* d, const void* k, const void* v, void* kc, void* vc,
+              cudaStream_t st) {
+    const int bh = d->batch * d->heads, nblk = d->seq_len / kBlock;
+    dim3 grid(nblk, bh);
+    if (d->head_dim == 64)
+        efta_encode_kv_kernel<64><<<grid, 256, 0, st>>>(
+            static_cast<const __half*>(k), static_cast<const __half*>(v), static_cast<__half*>(kc),
+            static_cast<__half*>(vc), d->seq_len, nblk);
+    else
+        efta_encode_kv_kernel<128><<<grid, 256, 0, st>>>(
+            static_cast<const __half*>(k), static_cast<const __half*>(v), static_cast<__half*>(kc),
+            static_cast<__half*>(vc), d->seq_len, nblk);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* efta_last_error(void) { return g_err.c_str(); }
+
+int efta_attn_validate(const efta_attn_desc* d) { return validate(d); }
+
+size_t efta_attn_workspace_bytes(const efta_attn_desc* d) {
+    if (validate(d)) return 0;
+    return ws_bytes(d);
+}
+
+float efta_flip_bit(float v, int width, int bit) {
+    // reference flip_bit (src/fault.cpp:27-37), 32-bit image only on the device path
+    uint32_t u;
+    std::memcpy(&u, &v, 4);
+    if (width != 32 || bit < 0 || bit > 31) return v;
+    u ^= (1u << bit);
+    std::memcpy(&v, &u, 4);
+    return v;
+}
+
+int efta_attn_encode_kv_f16(const efta_attn_desc* d, const uint16_t* k, const uint16_t* v,
+                            uint16_t* kc, uint16_t* vc, void* stream) {
+    if (int rc = validate(d)) return rc;
+    return encode_kv(d, k, v, kc, vc, static_cast<cudaStream_t>(stream));
+}
+
+int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t* k,
+                      const uint16_t* v, float* o, float* m_out, float* l_out, void* workspace,
+                      size_t workspace_bytes, const efta_fault_spec* faults, int n_faults,
+                      efta_event* events, int ev_cap, efta_fired* fired, int fired_cap,
+                      efta_counters* counters, void* stream) {
+    if (int rc = validate(d)) return rc;
+    if (!q || !k || !v || !o || !counters) return fail(1, "efta_attn_fwd_f16: null buffer");
+    if (n_faults > 0 && !d->debug)
+        return fail(1, "efta_attn_fwd_f16: fault injection needs the debug (tap) kernel variant");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int bh = d->batch * d->heads, nblk = d->seq_len / kBlock, D = d->head_dim;
+    const bool prot = d->mode != EFTA_MODE_NONE;
+    if (prot && (workspace == nullptr || workspace_bytes < ws_bytes(d)))
+        return fail(1, "efta_attn_fwd_f16: workspace too small");
+
+    CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(efta_counters), st));
+    uint16_t* kc = static_cast<uint16_t*>(workspace);
+    uint16_t* vc = kc ? kc + static_cast<size_t>(bh) * nblk * 32 * D : nullptr;
+    if (prot) {
+        if (int rc = encode_kv(d, k, v, kc, vc, st)) return rc;
+    }
+    CUtensorMap tq, tk, tv, tkc, tvc;
+    const uint64_t rows = static_cast<uint64_t>(bh) * d->seq_len;
+    bool ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, rows, D, 128) &&
+              make_map(&tv, v, rows, D, 128);
+    if (prot) {
+        ok = ok && make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 32) &&
+             make_map(&tvc, vc, static_cast<uint64_t>(bh) * nblk * 32, 128, 32);
+    } else {
+        tkc = tq;
+        tvc = tq;
+    }
+    if (!ok) return fail(2, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
+
+    AttnParams p{};
+    p.seq_len = d->seq_len;
+    p.nblk = nblk;
+    p.n_heads_flat = bh;
+    p.scale = d->scale == 0.0f ? 1.0f / std::sqrt(static_cast<float>(D)) : d->scale;
+    p.scale_log2 = p.scale * kLog2e;
+    p.rowmax_bias = d->rowmax_bias;
+    p.eps1 = d->eps1;
+    p.eps2 = d->eps2;
+    p.eps_lin = d->eps_lin;
+    p.o = o;
+    p.m_out = m_out;
+    p.l_out = l_out;
+    p.events = events;
+    p.ev_cap = events ? ev_cap : 0;
+    p.counters = counters;
+    p.faults = faults;
+    p.n_faults = faults ? n_faults : 0;
+    p.fired = fired;
+    p.fired_cap = fired ? fired_cap : 0;
+    p.observe_linear = d->observe_linear;
+    const bool dbg = d->debug != 0;
+    cudaError_t e = (D == 64) ? efta_launch_attn_d64(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st)
+                              : efta_launch_attn_d128(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
+    if (e != cudaSuccess) return fail(2, std::string("attention launch: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t* k,
+                           const uint16_t* v, float* o, float* m_out, float* l_out,
+                           const efta_fault_spec* faults, int n_faults, efta_event* events,
+                           int ev_cap, efta_fired* fired, int fired_cap, efta_counters* counters) {
+    if (int rc = validate(d)) return rc;
+    // per-thread device scratch, grown on demand and reused across calls
+    struct Scratch {
+        void* p = nullptr;
+        size_t n = 0;
+        ~Scratch() { if (p) cudaFree(p); }
+    };
+    thread_local Scratch s;
+    const size_t bh = static_cast<size_t>(d->batch) * d->heads;
+    const size_t n_in = bh * d->seq_len * d->head_dim;
+    const size_t bytes_in = n_in * 2, bytes_o = n_in * 4, bytes_ml = bh * d->seq_len * 4;
+    const size_t wsb = ws_bytes(d);
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t need = 3 * al(bytes_in) + al(bytes_o) + 2 * al(bytes_ml) + al(wsb) +
+                        al(sizeof(efta_counters)) + al(sizeof(efta_fault_spec) * (n_faults + 1)) +
+                        al(sizeof(efta_event) * (ev_cap + 1)) + al(sizeof(efta_fired) * (fired_cap + 1));
+    if (s.n < need) {
+        if (s.p) cudaFree(s.p);
+        s.p = nullptr;
+        s.n = 0;
+        CUDA_TRY(cudaMalloc(&s.p, need));
+        s.n = need;
+    }
+    char* base = static_cast<char*>(s.p);
+    auto take = [&](size_t b) { char* r = base; base += al(b); return r; };
+    uint16_t* dq = reinterpret_cast<uint16_t*>(take(bytes_in));
+    uint16_t* dk = reinterpret_cast<uint16_t*>(take(bytes_in));
+    uint16_t* dv = reinterpret_cast<uint16_t*>(take(bytes_in));
+    float* dout = reinterpret_cast<float*>(take(bytes_o));
+    float* dm = reinterpret_cast<float*>(take(bytes_ml));
+    float* dl = reinterpret_cast<float*>(take(bytes_ml));
+    void* dws = take(wsb);
+    efta_counters* dc = reinterpret_cast<efta_counters*>(take(sizeof(efta_counters)));
+    efta_fault_spec* df = reinterpret_cast<efta_fault_spec*>(take(sizeof(efta_fault_spec) * (n_faults + 1)));
+    efta_event* de = reinterpret_cast<efta_event*>(take(sizeof(efta_event) * (ev_cap + 1)));
+    efta_fired* dfi = reinterpret_cast<efta_fired*>(take(sizeof(efta_fired) * (fired_cap + 1)));
+    cudaStream_t st = 0;
+    CUDA_TRY(cudaMemcpyAsync(dq, q, bytes_in, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dk, k, bytes_in, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dv, v, bytes_in, cudaMemcpyHostToDevice, st));
+    if (n_faults > 0)
+        CUDA_TRY(cudaMemcpyAsync(df, faults, sizeof(efta_fault_spec) * n_faults, cudaMemcpyHostToDevice, st));
+    int rc = efta_attn_fwd_f16(d, dq, dk, dv, dout, dm, dl, dws, wsb, n_faults > 0 ? df : nullptr,
+                               n_faults, events ? de : nullptr, events ? ev_cap : 0,
+                               fired ? dfi : nullptr, fired ? fired_cap : 0, dc, st);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(o, dout, bytes_o, cudaMemcpyDeviceToHost, st));
+    if (m_out) CUDA_TRY(cudaMemcpyAsync(m_out, dm, bytes_ml, cudaMemcpyDeviceToHost, st));
+    if (l_out) CUDA_TRY(cudaMemcpyAsync(l_out, dl, bytes_ml, cudaMemcpyDeviceToHost, st));
+    efta_counters hc;
+    CUDA_TRY(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (counters) *counters = hc;
+    if (events && ev_cap > 0 && hc.n_events > 0)
+        CUDA_TRY(cudaMemcpy(events, de, sizeof(efta_event) * std::min(hc.n_events, ev_cap), cudaMemcpyDeviceToHost));
+    if (fired && fired_cap > 0 && hc.n_fired > 0)
+        CUDA_TRY(cudaMemcpy(fired, dfi, sizeof(efta_fired) * std::min(hc.n_fired, fired_cap), cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,16 @@
+// efta_launch.h — per-head-dim launchers of the fused attention kernel (defined in
+// efta_attn_inst.cu, one translation unit per head dim so they build in parallel).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "efta_attn.cuh"
+
+cudaError_t efta_launch_attn_d64(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMap& tk,
+                                 const CUtensorMap& tv, const CUtensorMap& tkc,
+                                 const CUtensorMap& tvc, const efta_sm100::AttnParams& p, int bh,
+                                 cudaStream_t st);
+cudaError_t efta_launch_attn_d128(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMap& tk,
+                                  const CUtensorMap& tv, const CUtensorMap& tkc,
+                                  const CUtensorMap& tvc, const efta_sm100::AttnParams& p, int bh,
+                                  cudaStream_t st);

@@ -1,0 +1,50 @@
+"""GPU parity of the fused sm_100a EFTA forward against the CPU oracle
+(oracle/efta_oracle.c, itself pinned bit-exact to the reference)."""
+import numpy as np
+import pytest
+
+from helpers import head_inputs, oracle, rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2  # north_star: max-rel-err <= 1e-2 for fp16 inputs / fp32 accumulation
+
+
+def _dev(x):
+    import torch
+    return torch.from_numpy(x).to(torch.float16).cuda().contiguous()
+
+
+@pytest.mark.parametrize("d,seq,heads", [(64, 512, 12), (128, 512, 4), (64, 1024, 2)])
+@pytest.mark.parametrize("mode", ["none", "efta-opt", "efta"])
+def test_forward_matches_oracle(d, seq, heads, mode):
+    from paper_2504_02211_b200 import efta_forward, Thresholds
+    q, k, v, _ = head_inputs(1234 + d + seq, heads, seq, d)
+    o, rep = efta_forward(_dev(q), _dev(k), _dev(v), mode=mode, thr=Thresholds(1e-4, 1e-3, 1e-3))
+    o = o.cpu().numpy()
+    m = rep.final_m.cpu().numpy()
+    l = rep.final_l.cpu().numpy()
+    orc = oracle()
+    for h in range(heads):
+        ref = orc.efta_forward(q[h], k[h], v[h], 128, 8, mode="none")
+        assert rel_err(o[h], ref.o) <= TOL, (h, rel_err(o[h], ref.o))
+        assert np.allclose(m[h], ref.m, rtol=1e-5, atol=1e-5)
+        assert np.allclose(l[h], ref.l, rtol=1e-3)
+    assert rep.detections == 0, rep.events[:4]
+    assert not rep.failed
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_protected_bit_identical_to_unprotected(d):
+    """Analog of reference acceptance check 2 (tests/acceptance.cpp:87-100):
+    the checksum side band leaves the main path bit-identical."""
+    from paper_2504_02211_b200 import efta_forward, Thresholds
+    q, k, v, _ = head_inputs(77 + d, 3, 512, d)
+    o0, r0 = efta_forward(_dev(q), _dev(k), _dev(v), mode="none")
+    thr = Thresholds(1e-4, 1e-3, 1e-3)
+    o1, r1 = efta_forward(_dev(q), _dev(k), _dev(v), mode="efta-opt", thr=thr)
+    o2, r2 = efta_forward(_dev(q), _dev(k), _dev(v), mode="efta", thr=thr)
+    assert (o0.view(-1).view(np.int32 if False else o0.dtype) == o1.view(-1)).all()
+    assert np.array_equal(o0.cpu().numpy().view(np.uint32), o1.cpu().numpy().view(np.uint32))
+    assert np.array_equal(o0.cpu().numpy().view(np.uint32), o2.cpu().numpy().view(np.uint32))
+    assert r1.detections == 0 and r2.detections == 0
