@@ -48,6 +48,8 @@ typedef struct {
     int observe_linear; /* KernelKnobs::observe_linear (efta.hpp:79) */
     float rowmax_bias;  /* KernelKnobs::rowmax_bias (efta.hpp:82) */
     int debug;          /* 1: fault-tap / observation kernel variant (required if n_faults > 0) */
+    int checksums_ready;/* 1: workspace already holds this K/V's checksum operands (skip the
+                           encode prepass; e.g. K/V reused across calls) */
 } efta_attn_desc;
 
 const char* efta_last_error(void);
@@ -76,6 +78,21 @@ int efta_attn_encode_kv_f16(const efta_attn_desc* d, const uint16_t* k, const ui
                             uint16_t* kc, uint16_t* vc, void* stream);
 
 float efta_flip_bit(float v, int width, int bit);
+
+/* ---- host-side helpers of the reference campaign (host memory only) ---- */
+/* trial_seed (include/efta/rng.hpp:55-58) */
+uint64_t efta_trial_seed(uint64_t base, uint64_t trial);
+/* Rng(seed); q,k,v = Matrix::random(n, d) as fp16 bits in that order, then, if
+ * n_sites > 0, sample_random_plan from the same stream (src/campaign.cpp:177-185,
+ * src/fault.cpp:143-164). spec->head is set to 0. */
+int efta_gen_trial_f16(uint64_t seed, int n, int d, int block, int stride, const int* sites,
+                       int n_sites, uint16_t* q, uint16_t* k, uint16_t* v, efta_fault_spec* spec);
+/* classify_trial (src/campaign.cpp:123-152); returns the Outcome enum value
+ * (campaign.hpp:12-20): 0 clean 1 false_alarm 2 corrected 3 range_restricted
+ * 4 masked_benign 5 range_contract 6 uncorrectable. */
+int efta_classify_trial(int rows, int cols, const float* out, const float* ref, int detections,
+                        int range_replacements, int failed, const float* final_l, int n_l,
+                        int plan_nonempty, int reduction_site, double eps2);
 
 #ifdef __cplusplus
 }

@@ -125,7 +125,7 @@ class FTReport:
 def _desc(b, h, s, d, mode, thr, scale, observe_linear, rowmax_bias, debug, block, stride):
     return _lib.AttnDesc(b, h, s, d, block, stride, float(scale), MODES[mode], float(thr.eps1),
                          float(thr.eps2), float(thr.eps_lin), 1 if observe_linear else 0,
-                         float(rowmax_bias), 1 if debug else 0)
+                         float(rowmax_bias), 1 if debug else 0, 0)
 
 
 def _as_bhsd(x: torch.Tensor):

@@ -1,0 +1,166 @@
+"""GPU-backed fault-injection campaign — mirror of the reference's run_campaign /
+classify_trial / calibrate_thresholds (reference src/campaign.cpp:123-297).
+
+Trials are batched: every (trial, head) record of the reference becomes one
+head of a single batched launch (heads are independent units), inputs and
+fault plans are drawn with the reference's Rng stream (efta_gen_trial_f16, the
+C++ host layer), and outcomes are classified on the host by the reference's
+outcome ladder (efta_classify_trial).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import SITES, lib
+from .attention import EftaAttention, FaultSpec, Thresholds
+
+OUTCOMES = ["clean", "false_alarm", "corrected", "range_restricted", "masked_benign",
+            "range_contract", "uncorrectable"]
+
+lib.efta_trial_seed.restype = C.c_uint64
+lib.efta_trial_seed.argtypes = [C.c_uint64, C.c_uint64]
+lib.efta_gen_trial_f16.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_int), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.POINTER(_lib.FaultSpec)]
+lib.efta_classify_trial.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                    C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double]
+
+
+def trial_seed(base: int, trial: int) -> int:
+    return int(lib.efta_trial_seed(base, trial))
+
+
+def gen_head(seed: int, n: int, d: int, block=128, stride=8, sites=None):
+    """Reference Rng(seed): q, k, v = Matrix::random(n, d) in that order, then an
+    optional sample_random_plan (src/campaign.cpp:177-185)."""
+    q = np.empty((n, d), np.uint16)
+    k = np.empty_like(q)
+    v = np.empty_like(q)
+    sites = list(sites or [])
+    arr = (C.c_int * max(1, len(sites)))(*sites)
+    spec = _lib.FaultSpec()
+    rc = lib.efta_gen_trial_f16(seed, n, d, block, stride, arr, len(sites), q.ctypes.data,
+                                k.ctypes.data, v.ctypes.data, C.byref(spec))
+    if rc:
+        raise _lib.ConfigError("gen_trial failed")
+    f = None
+    if sites:
+        f = FaultSpec(spec.site, spec.block_i, spec.block_j, spec.row, spec.col, spec.bit,
+                      spec.trigger)
+    return q.view(np.float16), k.view(np.float16), v.view(np.float16), f
+
+
+def classify(out: np.ndarray, ref: np.ndarray, detections: int, range_replacements: int,
+             failed: bool, final_l: np.ndarray, spec, eps2: float) -> str:
+    out = np.ascontiguousarray(out, np.float32)
+    ref = np.ascontiguousarray(ref, np.float32)
+    fl = np.ascontiguousarray(final_l, np.float32)
+    red = spec is not None and spec.site in (SITES.index("REDUCE_MAX"), SITES.index("REDUCE_SUM"))
+    o = lib.efta_classify_trial(out.shape[0], out.shape[1], out.ctypes.data, ref.ctypes.data,
+                                detections, range_replacements, 1 if failed else 0, fl.ctypes.data,
+                                fl.size, 1 if spec is not None else 0, 1 if red else 0, eps2)
+    return OUTCOMES[o]
+
+
+def per_head_report(events, n_heads):
+    """Split device events by head (the device logs non-CLEAN events only)."""
+    det = [0] * n_heads
+    rr = [0] * n_heads
+    failed = [False] * n_heads
+    for e in events:
+        h = e["head"]
+        if e["status"] != "clean":
+            det[h] += 1
+        if e["kind"] == "rowsum_range":
+            rr[h] += e["corrections"]
+        if e["status"] in ("detected_uncorrectable", "nonfinite"):
+            failed[h] = True
+    return det, rr, failed
+
+
+def calibrate_thresholds(seq_len, head_dim, mode="efta-opt", trials=64, safety=2.0, seed=1,
+                         device="cuda"):
+    """calibrate_thresholds (src/campaign.cpp:261-297) on the GPU: clean runs in
+    observation mode (+ per-iteration linear residuals); each threshold is the worst
+    clean residual of its family times `safety`. Trials run as heads of one launch."""
+    qs, ks, vs = [], [], []
+    for t in range(trials):
+        q, k, v, _ = gen_head(trial_seed(seed, t), seq_len, head_dim)
+        qs.append(q); ks.append(k); vs.append(v)
+    dev = torch.device(device)
+    q = torch.from_numpy(np.stack(qs)).to(dev).view(1, trials, seq_len, head_dim)
+    k = torch.from_numpy(np.stack(ks)).to(dev).view(1, trials, seq_len, head_dim)
+    v = torch.from_numpy(np.stack(vs)).to(dev).view(1, trials, seq_len, head_dim)
+    op = EftaAttention(1, trials, seq_len, head_dim, mode=mode, thr=Thresholds.observe(),
+                       observe_linear=True, debug=True, device=dev)
+    op(q, k, v)
+    rep = op.report()
+    fe, fo, fl = rep.family_max
+    thr = Thresholds(fe * safety if fe > 0 else math.inf, fo * safety if fo > 0 else math.inf,
+                     fl * safety if fl > 0 else math.inf)
+    return thr, rep.family_max
+
+
+def run_gpu_campaign(n_trials=20, heads=12, seq_len=512, head_dim=64, sites=None, seed=7,
+                     mode="efta-opt", thr: Thresholds | None = None, calibrate_trials=128,
+                     device="cuda", fixed_plan=None):
+    """run_campaign (src/campaign.cpp:154-259) with injection: one single-bit
+    fault per (trial, head) record, classified against the fault-free twin."""
+    if sites is None:
+        sites = list(range(8))
+    if thr is None:
+        thr, _ = calibrate_thresholds(seq_len, head_dim, mode, calibrate_trials, 2.0,
+                                      seed ^ 0xCA11B7A7, device)
+    n_rec = n_trials * heads
+    qs, ks, vs, specs = [], [], [], []
+    for t in range(n_trials):
+        tseed = trial_seed(seed, t)
+        for h in range(heads):
+            hseed = tseed if heads == 1 else trial_seed(tseed, h)
+            q, k, v, f = gen_head(hseed, seq_len, head_dim, sites=None if fixed_plan else sites)
+            if fixed_plan is not None:
+                f = FaultSpec.parse(fixed_plan) if isinstance(fixed_plan, str) else fixed_plan
+                f = FaultSpec(f.site, f.block_i, f.block_j, f.row, f.col, f.bit, f.trigger)
+            f.head = t * heads + h
+            qs.append(q); ks.append(k); vs.append(v); specs.append(f)
+    dev = torch.device(device)
+    shape = (1, n_rec, seq_len, head_dim)
+    q = torch.from_numpy(np.stack(qs)).to(dev).view(shape)
+    k = torch.from_numpy(np.stack(ks)).to(dev).view(shape)
+    v = torch.from_numpy(np.stack(vs)).to(dev).view(shape)
+    ev_cap = max(4096, 64 * n_rec)
+    clean = EftaAttention(1, n_rec, seq_len, head_dim, mode=mode, thr=thr, debug=True,
+                          ev_cap=ev_cap, device=dev)
+    o_ref, _, _ = clean(q, k, v)
+    rep_clean = clean.report()
+    faulted = EftaAttention(1, n_rec, seq_len, head_dim, mode=mode, thr=thr, debug=True,
+                            ev_cap=ev_cap, fired_cap=2 * n_rec, device=dev)
+    faulted.set_faults(specs)
+    o, m, l = faulted(q, k, v)
+    rep = faulted.report(m, l)
+    det, rr, failed = per_head_report(rep.events, n_rec)
+    fired_heads = {f["spec"].head for f in rep.fired}
+    o_np = o.view(n_rec, seq_len, head_dim).cpu().numpy()
+    r_np = o_ref.view(n_rec, seq_len, head_dim).cpu().numpy()
+    l_np = l.view(n_rec, seq_len).cpu().numpy()
+    records = []
+    stats = {k2: 0 for k2 in OUTCOMES}
+    for i in range(n_rec):
+        out = classify(o_np[i], r_np[i], det[i], rr[i], failed[i], l_np[i], specs[i], thr.eps2)
+        stats[out] += 1
+        records.append(dict(trial=i // heads, head=i % heads, fault=specs[i].to_string(),
+                            fired=i in fired_heads, detections=det[i], outcome=out,
+                            residual_out=float(np.abs(o_np[i].astype(np.float64) - r_np[i]).max())))
+    n_fired = sum(r["fired"] for r in records)
+    bad = sum(1 for r in records if r["fired"] and r["outcome"] == "uncorrectable")
+    return {"records": n_rec, "fired": n_fired, "coverage": 1.0 - bad / n_fired if n_fired else 1.0,
+            "corrected": stats["corrected"], "masked_benign": stats["masked_benign"],
+            "range_restricted": stats["range_restricted"],
+            "range_contract": stats["range_contract"], "uncorrectable": stats["uncorrectable"],
+            "false_alarms": rep_clean.detections, "thresholds": (thr.eps1, thr.eps2, thr.eps_lin),
+            "detail": records, "events": rep.events}

@@ -156,7 +156,7 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(efta_counters), st));
     uint16_t* kc = static_cast<uint16_t*>(workspace);
     uint16_t* vc = kc ? kc + static_cast<size_t>(bh) * nblk * 32 * D : nullptr;
-    if (prot) {
+    if (prot && !d->checksums_ready) {
         if (int rc = encode_kv(d, k, v, kc, vc, st)) return rc;
     }
     CUtensorMap tq, tk, tv, tkc, tvc;
