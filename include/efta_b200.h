@@ -73,7 +73,7 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
                            int ev_cap, efta_fired* fired, int fired_cap, efta_counters* counters);
 
 /* Strided checksum operands of K and V only (the encode prepass the forward runs
- * internally); kc: [BH*nblk*32, head_dim] fp16, vc: [BH*nblk*32, 128] fp16. */
+ * internally); kc: [BH*nblk*32, head_dim] fp16, vc: [BH*nblk*128, 64] fp16. */
 int efta_attn_encode_kv_f16(const efta_attn_desc* d, const uint16_t* k, const uint16_t* v,
                             uint16_t* kc, uint16_t* vc, void* stream);
 

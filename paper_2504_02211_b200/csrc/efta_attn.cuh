@@ -15,16 +15,17 @@
 //               epilogue normalisation + final output check + store.
 //
 // TMEM columns (512 allocated):
-//   S[b]   = b*128     (b = j&1; P_j (fp16x2) is written over its first 64 cols)
-//   Scs[b] = 256+16b   (16 cols: c1[0..7] c2[0..7] of S = Q.[KC_hi;KC_lo]^T)
-//   O      = 288       (D cols), Ocs = 288+D (16 cols: strided checksums of O)
+//   S[b] = b*160 (b = j&1): 128 score cols | 16 hi | 16 lo checksum cols
+//          (P_j as fp16x2 is written over its first 64 cols)
+//   O    = 320: D cols | 16 hi | 16 lo checksum cols
 //
 // Checksum operands (hi/lo fp16 split of the fp32 strided sums, produced by
-// efta_encode_kv in efta_encode.cu) ride alongside every K/V tile:
+// efta_encode_kv in efta_encode.cuh) ride alongside every K/V tile:
 //   KC_j  [32 x D]   rows 0-7 c1_hi, 8-15 c2_hi, 16-23 c1_lo, 24-31 c2_lo
-//   VC_j  [32 x 128] same row order, columns = keys of the block
-// so S's checksum columns come out of the same tcgen05 pipe as S (two N=16
-// MMAs accumulating hi then lo) and O's checksum columns out of the PV MMAs.
+//   VC_j  [128 x 64] per key: cols 0-7 c1_hi, 8-15 c2_hi, 16-23 c1_lo, 24-31 c2_lo, 32-63 zero
+// They are appended to the B operands so a single tcgen05.mma per k-step computes
+// the scores plus their checksums (N = 160) and P.V plus the output checksums
+// (N = D + 32): every operand is read from SMEM/TMEM exactly once.
 #pragma once
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -57,6 +58,8 @@ struct AttnParams {
     efta_fired* fired;
     int fired_cap;
     int observe_linear;
+    // exp-stage bracket: |ln(prod/pc1)| > eps1  <=>  prod outside [pc1*exp_lo, pc1*exp_hi]
+    float exp_lo, exp_hi;
 };
 
 template <int D>
@@ -64,13 +67,18 @@ struct AttnLayout {
     static constexpr int NSUB = D / 64;
     static constexpr int KS = (D == 64) ? 3 : 2;  // K ring stages
     static constexpr int VS = (D == 64) ? 3 : 2;  // V ring stages
+    // K stage: per 64-column chunk [K_j rows 0..127 | KC rows 0..31] so that one
+    // K-major B descriptor spans N = 128 (+32 checksum rows) = 160
+    static constexpr uint32_t K_SUB = 16384 + 4096;
+    static constexpr uint32_t K_STAGE = NSUB * K_SUB;
+    // V stage: MN-major [V chunk 0 | V chunk 1 | VC (32 used of 64 cols)], 16 KB each,
+    // so one MN-major B descriptor spans N = D (+32 checksum columns)
+    static constexpr uint32_t V_STAGE = (NSUB + 1) * 16384;
     static constexpr uint32_t Q_BYTES = NSUB * 16384;
     static constexpr uint32_t K_BYTES = NSUB * 16384;
     static constexpr uint32_t KC_BYTES = NSUB * 4096;
     static constexpr uint32_t V_BYTES = NSUB * 16384;
-    static constexpr uint32_t VC_BYTES = 2 * 4096;
-    static constexpr uint32_t K_STAGE = K_BYTES + KC_BYTES;
-    static constexpr uint32_t V_STAGE = V_BYTES + VC_BYTES;
+    static constexpr uint32_t VC_BYTES = 16384;
     static constexpr uint32_t OFF_Q = 0;
     static constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
     static constexpr uint32_t OFF_V = OFF_K + KS * K_STAGE;
@@ -82,7 +90,10 @@ struct AttnLayout {
     static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
     static constexpr uint32_t RED_BYTES = 128 * 24 + 256;  // RowSlot[128] + ints + doubles
     static constexpr uint32_t SMEM_BYTES = OFF_RED + RED_BYTES + 1024;  // + alignment slack
-    static constexpr uint32_t COL_S0 = 0, COL_SCS0 = 256, COL_O = 288, COL_OCS = 288 + D;
+    // TMEM: S[b] = b*160: cols 0..127 scores (P aliased over 0..63), 128..143 checksum
+    // hi-products, 144..159 lo-products; O at 320: D cols + 16 hi + 16 lo checksum cols.
+    static constexpr uint32_t S_STRIDE = 160;
+    static constexpr uint32_t COL_S0 = 0, COL_O = 320;
     static constexpr uint32_t TMEM_COLS = 512;
 };
 

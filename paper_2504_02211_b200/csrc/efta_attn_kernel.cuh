@@ -42,13 +42,15 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                 sc[c4 * 32 + x] = __fmul_rn(__uint_as_float(r[x]), p.scale);
             }
         }
-        uint32_t q[16];
-        tmem_ld16(cs_addr, q);
+        uint32_t qh[16], ql[16];
+        tmem_ld16(cs_addr, qh);
+        tmem_ld16(cs_addr + 16, ql);
         tmem_wait_ld();
 #pragma unroll
         for (int x = 0; x < kStride; ++x) {
-            c1s[x] = __fmul_rn(__uint_as_float(q[x]), p.scale);
-            c2s[x] = __fmul_rn(__uint_as_float(q[kStride + x]), p.scale);
+            c1s[x] = __fmul_rn(__fadd_rn(__uint_as_float(qh[x]), __uint_as_float(ql[x])), p.scale);
+            c2s[x] = __fmul_rn(__fadd_rn(__uint_as_float(qh[kStride + x]), __uint_as_float(ql[kStride + x])),
+                               p.scale);
         }
     }
     if (DBG && sc_fault_col >= 0) sc[sc_fault_col] = sc_fault_val;  // GEMM1_OUT upset lives in sc
@@ -343,13 +345,11 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                 uint8_t* dst = smem + L::OFF_K + s * L::K_STAGE;
                 mbar_arrive_expect_tx(&k_full[s], L::K_BYTES + (PROT ? L::KC_BYTES : 0));
 #pragma unroll
-                for (int sub = 0; sub < NSUB; ++sub)
-                    tma_load_2d(dst + sub * 16384, &tm_k, &k_full[s], sub * 64, seq_row0 + j * kBlock,
-                                kEvictLast);
-                if (PROT) {
-#pragma unroll
-                    for (int sub = 0; sub < NSUB; ++sub)
-                        tma_load_2d(dst + L::K_BYTES + sub * 4096, &tm_kc, &k_full[s], sub * 64,
+                for (int sub = 0; sub < NSUB; ++sub) {
+                    tma_load_2d(dst + sub * L::K_SUB, &tm_k, &k_full[s], sub * 64,
+                                seq_row0 + j * kBlock, kEvictLast);
+                    if (PROT)
+                        tma_load_2d(dst + sub * L::K_SUB + 16384, &tm_kc, &k_full[s], sub * 64,
                                     (head * n + j) * 32, kEvictLast);
                 }
             }
@@ -371,20 +371,17 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                 for (int sub = 0; sub < NSUB; ++sub)
                     tma_load_2d(dst + sub * 16384, &tm_v, &v_full[s], sub * 64, seq_row0 + j * kBlock,
                                 kEvictLast);
-                if (PROT) {
-#pragma unroll
-                    for (int sub = 0; sub < 2; ++sub)
-                        tma_load_2d(dst + L::V_BYTES + sub * 4096, &tm_vc, &v_full[s], sub * 64,
-                                    (head * n + j) * 32, kEvictLast);
-                }
+                if (PROT)
+                    tma_load_2d(dst + NSUB * 16384, &tm_vc, &v_full[s], 0, (head * n + j) * kBlock,
+                                kEvictLast);
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {
-            constexpr uint32_t ID_S = idesc_f16_f32(128, 128, 0, 0);
-            constexpr uint32_t ID_CS = idesc_f16_f32(128, 16, 0, 0);
-            constexpr uint32_t ID_PV = idesc_f16_f32(128, D, 0, 1);
+            // protected: N grows by the 32 checksum rows/cols (hi + lo products)
+            constexpr uint32_t ID_S = idesc_f16_f32(128, PROT ? 160 : 128, 0, 0);
+            constexpr uint32_t ID_PV = idesc_f16_f32(128, PROT ? D + 32 : D, 0, 1);
             mbar_wait(q_full, 0);
             tc_fence_after();
             auto issue_s = [&](int j) {
@@ -392,25 +389,13 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                 mbar_wait(&k_full[s], (j / KS) & 1);
                 tc_fence_after();
                 const uint32_t kb = k_smem + s * L::K_STAGE;
-                const uint32_t d_s = tmem + L::COL_S0 + (j & 1) * 128;
+                const uint32_t d_s = tmem + L::COL_S0 + (j & 1) * L::S_STRIDE;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    mma_ss(d_s, smem_desc_sw128(q_smem + off, 16, 1024),
-                           smem_desc_sw128(kb + off, 16, 1024), ID_S, kk > 0);
-                }
-                if (PROT) {
-                    const uint32_t d_cs = tmem + L::COL_SCS0 + (j & 1) * 16;
-                    const uint32_t kcb = kb + L::K_BYTES;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk) {
-                            const uint32_t offq = (kk >> 2) * 16384 + (kk & 3) * 32;
-                            const uint32_t offc = (kk >> 2) * 4096 + h * 2048 + (kk & 3) * 32;
-                            mma_ss(d_cs, smem_desc_sw128(q_smem + offq, 16, 1024),
-                                   smem_desc_sw128(kcb + offc, 16, 1024), ID_CS, (h | kk) > 0);
-                        }
+                    const uint32_t offq = (kk >> 2) * 16384 + (kk & 3) * 32;
+                    const uint32_t offk = (kk >> 2) * L::K_SUB + (kk & 3) * 32;
+                    mma_ss(d_s, smem_desc_sw128(q_smem + offq, 16, 1024),
+                           smem_desc_sw128(kb + offk, 16, 1024), ID_S, kk > 0);
                 }
                 tc_commit(&k_empty[s]);
                 tc_commit(&s_full[j & 1]);
@@ -424,23 +409,12 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                 mbar_wait(&v_full[s], (j / VS) & 1);
                 tc_fence_after();
                 const uint32_t vb = v_smem + s * L::V_STAGE;
-                const uint32_t a_p = tmem + L::COL_S0 + (j & 1) * 128;
+                const uint32_t a_p = tmem + L::COL_S0 + (j & 1) * L::S_STRIDE;
                 const uint32_t acc0 = (j > 0 || DBG) ? 1u : 0u;
 #pragma unroll
                 for (int kk = 0; kk < kBlock / 16; ++kk)
                     mma_ts(tmem + L::COL_O, a_p + kk * 8, smem_desc_sw128(vb + kk * 2048, 16384, 1024),
                            ID_PV, acc0 | (kk > 0));
-                if (PROT) {
-                    const uint32_t vcb = vb + L::V_BYTES;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int kk = 0; kk < kBlock / 16; ++kk) {
-                            const uint32_t offc = (kk >> 2) * 4096 + h * 2048 + (kk & 3) * 32;
-                            mma_ts(tmem + L::COL_OCS, a_p + kk * 8, smem_desc_sw128(vcb + offc, 16, 1024),
-                                   ID_CS, acc0 | (h | kk) > 0);
-                        }
-                }
                 tc_commit(&v_empty[s]);
                 tc_commit(o_done);
             }
@@ -478,17 +452,25 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
 
         for (int j = 0; j < n; ++j) {
             const int b = j & 1;
-            const uint32_t s_addr = lane_base + L::COL_S0 + b * 128;
-            const uint32_t cs_addr = lane_base + L::COL_SCS0 + b * 16;
+            const uint32_t s_addr = lane_base + L::COL_S0 + b * L::S_STRIDE;
+            const uint32_t cs_addr = s_addr + 128;  // 16 hi + 16 lo checksum product cols
             mbar_wait(&s_full[b], (j >> 1) & 1);
             tc_fence_after();
             float pv[kBlock];
-            uint32_t csr[16];
+            uint32_t csr[16], csl[16];
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4)
                 tmem_ld32(s_addr + c4 * 32, *reinterpret_cast<uint32_t(*)[32]>(&pv[c4 * 32]));
-            if (PROT) tmem_ld16(cs_addr, csr);
+            if (PROT) {
+                tmem_ld16(cs_addr, csr);
+                tmem_ld16(cs_addr + 16, csl);
+            }
             tmem_wait_ld();
+            if (PROT) {
+#pragma unroll
+                for (int x = 0; x < 16; ++x)
+                    csr[x] = __float_as_uint(__fadd_rn(__uint_as_float(csr[x]), __uint_as_float(csl[x])));
+            }
 
             float bm, m_new;
             int sc_fault_col = -1;
@@ -546,40 +528,53 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                 bm = __fmul_rn(fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)), scale) + p.rowmax_bias;
                 m_new = (m_run < bm) ? bm : m_run;
                 const float mL = m_new * kLog2e;
+                const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
 #pragma unroll
-                for (int c = 0; c < kBlock; ++c) pv[c] = ex2_approx(fmaf(pv[c], scale_log2, -mL));
+                for (int c = 0; c < kBlock; c += 2) {
+                    const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
+                    pv[c] = ex2_approx(a.x);
+                    pv[c + 1] = ex2_approx(a.y);
+                }
             }
 
-            // ---- exp-domain strided product check (SNVR; snvr.cpp:52-83)
+            // ---- exp-domain strided product check (SNVR; snvr.cpp:52-83):
+            // group x: prod_l P[x + 8l] vs Pc1 = exp(scale*c1 - 16 m); the reference's
+            // log-domain test |sum log P - log Pc1| > eps1 becomes the bracket
+            // prod outside [Pc1 e^-eps1, Pc1 e^eps1] (no log on the fast path).
+            const float f = ex2_approx((m_run - m_new) * kLog2e);
             bool exp_affected = false, factor_bad = false;
             float exp_res = 0.0f;
             int exp_viol = 0;
             if (PROT) {
-                float prod[kStride];
+                float2 prod[kStride / 2];
 #pragma unroll
-                for (int x = 0; x < kStride; ++x) prod[x] = pv[x];
+                for (int x = 0; x < kStride / 2; ++x) prod[x] = make_float2(pv[2 * x], pv[2 * x + 1]);
 #pragma unroll
-                for (int c = kStride; c < kBlock; ++c) prod[c % kStride] = __fmul_rn(prod[c % kStride], pv[c]);
+                for (int l = 1; l < kBlock / kStride; ++l)
+#pragma unroll
+                    for (int x = 0; x < kStride / 2; ++x)
+                        prod[x] = fmul2(prod[x], make_float2(pv[kStride * l + 2 * x], pv[kStride * l + 2 * x + 1]));
                 const float g16m = 16.0f * m_new;
                 bool degenerate = !isfinite(m_new);
 #pragma unroll
                 for (int x = 0; x < kStride; ++x) {
+                    const float pr = (x & 1) ? prod[x >> 1].y : prod[x >> 1].x;
                     const float c1s = __fmul_rn(__uint_as_float(csr[x]), scale);
                     const float pc1 = ex2_approx(__fsub_rn(c1s, g16m) * kLog2e);
-                    if (!(prod[x] > 0.0f && prod[x] < CUDART_INF_F) || !(pc1 > 0.0f && pc1 < CUDART_INF_F)) {
-                        degenerate = true;
-                    } else {
-                        const float d = fabsf(lg2_approx(__fdividef(prod[x], pc1))) * kLn2;
-                        exp_res = fmaxf(exp_res, d);
-                        if (d > p.eps1) { exp_affected = true; ++exp_viol; }
+                    const bool bad = !(pr >= pc1 * p.exp_lo && pr <= pc1 * p.exp_hi);
+                    if (DBG) {
+                        if (!(pr > 0.0f && pr < CUDART_INF_F) || !(pc1 > 0.0f && pc1 < CUDART_INF_F)) {
+                            degenerate = true;
+                        } else {
+                            const float d = fabsf(lg2_approx(__fdividef(pr, pc1))) * kLn2;
+                            exp_res = fmaxf(exp_res, d);
+                        }
                     }
+                    if (bad) { exp_affected = true; ++exp_viol; }
                 }
                 if (degenerate) { exp_affected = true; exp_res = CUDART_INF_F; exp_viol = 1; }
-                if (j > 0) {
-                    const float f = ex2_approx((m_run - m_new) * kLog2e);
-                    factor_bad = !(isfinite(f) && f > 0.0f && f <= 1.0f);
-                }
-                if (isfinite(exp_res)) fam_exp = fmaxf(fam_exp, exp_res);
+                if (j > 0) factor_bad = !(f > 0.0f && f <= 1.0f);  // NaN fails both
+                if (DBG && isfinite(exp_res)) fam_exp = fmaxf(fam_exp, exp_res);
                 if (named_bar_or(6, 128, exp_affected || factor_bad)) {
                     float p_loc[kBlock];
 #pragma unroll
@@ -596,17 +591,15 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
             }
 
             // ---- rescale factor, lower bound, denominator (efta.cpp:192-242)
-            const float f = ex2_approx((m_run - m_new) * kLog2e);
-            if (PROT) lb = __fadd_rn(__fmul_rn(lb, f), ex2_approx((bm - m_new) * kLog2e));
-            float ps0 = 0.0f, ps1 = 0.0f, ps2 = 0.0f, ps3 = 0.0f;
+            const float fr = PROT ? ex2_approx((m_run - m_new) * kLog2e) : f;  // m_new may be repaired
+            if (PROT) lb = __fadd_rn(__fmul_rn(lb, fr), ex2_approx((bm - m_new) * kLog2e));
+            float2 ps0 = make_float2(pv[0], pv[1]), ps1 = make_float2(pv[2], pv[3]);
 #pragma unroll
-            for (int c = 0; c < kBlock; c += 4) {
-                ps0 += pv[c];
-                ps1 += pv[c + 1];
-                ps2 += pv[c + 2];
-                ps3 += pv[c + 3];
+            for (int c = 4; c < kBlock; c += 4) {
+                ps0 = fadd2(ps0, make_float2(pv[c], pv[c + 1]));
+                ps1 = fadd2(ps1, make_float2(pv[c + 2], pv[c + 3]));
             }
-            l_run = __fadd_rn(__fmul_rn(f, l_run), (ps0 + ps1) + (ps2 + ps3));
+            l_run = __fadd_rn(__fmul_rn(fr, l_run), (ps0.x + ps0.y) + (ps1.x + ps1.y));
             if (DBG) l_run = tap(p, EFTA_REDUCE_SUM, j, 0, l_run);
 
             // ---- P (fp16) over the S columns it came from
@@ -627,12 +620,17 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                 if (MODE == EFTA_MODE_EFTA) {
                     // per-iteration output check of the accumulator after GEMM II of j-1
                     float o[D];
-                    uint32_t oc[16];
+                    uint32_t oc[32];
 #pragma unroll
                     for (int c = 0; c < D / 32; ++c)
                         tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
-                    tmem_ld16(lane_base + L::COL_OCS, oc);
+                    tmem_ld32(lane_base + L::COL_O + D, oc);
                     tmem_wait_ld();
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) {
+                        oc[x] = __float_as_uint(__fadd_rn(__uint_as_float(oc[x]), __uint_as_float(oc[16 + x])));
+                        oc[16 + x] = 0u;
+                    }
                     if (DBG) {
 #pragma unroll
                         for (int c = 0; c < D; ++c) o[c] = tap(p, EFTA_GEMM2_ACC, j - 1, c, o[c]);
@@ -644,20 +642,20 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                     verify_output_tile<D>(p, o, c1, c2, p.eps2, head, qt, j - 1, row, rs, res);
                     if (isfinite(res)) fam_out = fmaxf(fam_out, res);
 #pragma unroll
-                    for (int c = 0; c < D; ++c) o[c] = __fmul_rn(o[c], f);
+                    for (int c = 0; c < D; ++c) o[c] = __fmul_rn(o[c], fr);
                     if (DBG) {
 #pragma unroll
                         for (int c = 0; c < D; ++c) o[c] = tap(p, EFTA_RESCALE_FACTOR, j, c, o[c]);
                     }
 #pragma unroll
-                    for (int x = 0; x < kStride; ++x) { oc[x] = __float_as_uint(__fmul_rn(c1[x], f)); oc[kStride + x] = __float_as_uint(__fmul_rn(c2[x], f)); }
+                    for (int x = 0; x < kStride; ++x) { oc[x] = __float_as_uint(__fmul_rn(c1[x], fr)); oc[kStride + x] = __float_as_uint(__fmul_rn(c2[x], fr)); }
 #pragma unroll
                     for (int c = 0; c < D / 32; ++c)
                         tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
-                    tmem_st16(lane_base + L::COL_OCS, oc);
+                    tmem_st32(lane_base + L::COL_O + D, oc);
                 } else {
-                    const bool need = DBG || !__all_sync(0xffffffffu, f == 1.0f);
-                    if (need) {
+                    const bool need = DBG || !__all_sync(0xffffffffu, fr == 1.0f);
+                    if (need && DBG) {
 #pragma unroll
                         for (int c = 0; c < D / 32; ++c) {
                             float o[32];
@@ -665,22 +663,34 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                             tmem_wait_ld();
 #pragma unroll
                             for (int x = 0; x < 32; ++x) {
-                                float v = o[x];
-                                if (DBG) v = tap(p, EFTA_GEMM2_ACC, j - 1, c * 32 + x, v);
-                                v = __fmul_rn(v, f);
-                                if (DBG) v = tap(p, EFTA_RESCALE_FACTOR, j, c * 32 + x, v);
-                                o[x] = v;
+                                float v = tap(p, EFTA_GEMM2_ACC, j - 1, c * 32 + x, o[x]);
+                                v = __fmul_rn(v, fr);
+                                o[x] = tap(p, EFTA_RESCALE_FACTOR, j, c * 32 + x, v);
                             }
                             tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
                         }
-                        if (PROT) {
-                            float oc[16];
-                            tmem_ld16(lane_base + L::COL_OCS, *reinterpret_cast<uint32_t(*)[16]>(&oc[0]));
-                            tmem_wait_ld();
+                    }
+                    if (need) {
+                        // all chunks in flight at once (P's registers are free by now)
+                        constexpr int NCH = DBG ? (PROT ? 1 : 0) : (D / 32 + (PROT ? 1 : 0));
+                        constexpr int C0 = DBG ? D / 32 : 0;
+                        float o[NCH > 0 ? NCH : 1][32];
 #pragma unroll
-                            for (int x = 0; x < 16; ++x) oc[x] = __fmul_rn(oc[x], f);
-                            tmem_st16(lane_base + L::COL_OCS, *reinterpret_cast<uint32_t(*)[16]>(&oc[0]));
-                        }
+                        for (int c = 0; c < NCH; ++c)
+                            tmem_ld32(lane_base + L::COL_O + (C0 + c) * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
+                        tmem_wait_ld();
+                        const float2 f2 = make_float2(fr, fr);
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                            for (int x = 0; x < 32; x += 2) {
+                                const float2 r2 = fmul2(make_float2(o[c][x], o[c][x + 1]), f2);
+                                o[c][x] = r2.x;
+                                o[c][x + 1] = r2.y;
+                            }
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c)
+                            tmem_st32(lane_base + L::COL_O + (C0 + c) * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
                     }
                 }
             } else if (DBG) {
@@ -692,10 +702,10 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                     for (int x = 0; x < 32; ++x) o[x] = tap(p, EFTA_RESCALE_FACTOR, 0, c * 32 + x, 0.0f);
                     tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
                 }
-                uint32_t z[16];
+                uint32_t z[32];
 #pragma unroll
-                for (int x = 0; x < 16; ++x) z[x] = 0u;
-                tmem_st16(lane_base + L::COL_OCS, z);
+                for (int x = 0; x < 32; ++x) z[x] = 0u;
+                tmem_st32(lane_base + L::COL_O + D, z);
             }
             tmem_wait_st();
             tc_fence_before();
@@ -712,13 +722,14 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         for (int c = 0; c < D / 32; ++c)
             tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
         {
-            uint32_t oc[16];
-            if (PROT) tmem_ld16(lane_base + L::COL_OCS, oc);
+            uint32_t oc[32];
+            if (PROT) tmem_ld32(lane_base + L::COL_O + D, oc);
             tmem_wait_ld();
 #pragma unroll
             for (int x = 0; x < kStride; ++x) {
-                c1[x] = PROT ? __uint_as_float(oc[x]) : 0.0f;
-                c2[x] = PROT ? __uint_as_float(oc[kStride + x]) : 0.0f;
+                c1[x] = PROT ? __fadd_rn(__uint_as_float(oc[x]), __uint_as_float(oc[16 + x])) : 0.0f;
+                c2[x] = PROT ? __fadd_rn(__uint_as_float(oc[kStride + x]), __uint_as_float(oc[16 + kStride + x]))
+                             : 0.0f;
             }
         }
         if (DBG) {

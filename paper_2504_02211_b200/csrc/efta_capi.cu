@@ -90,7 +90,7 @@ int validate(const efta_attn_desc* d) {
 size_t ws_bytes(const efta_attn_desc* d) {
     const size_t bh = static_cast<size_t>(d->batch) * d->heads;
     const size_t nblk = d->seq_len / kBlock;
-    return bh * nblk * 32 * (d->head_dim + 128) * sizeof(__half) + 256;
+    return bh * nblk * (32 * d->head_dim + 128 * 64) * sizeof(__half) + 256;
 }
 
 int encode_kv(const efta_attn_desc* d, const void* k, const void* v, void* kc, void* vc,
@@ -165,7 +165,7 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
               make_map(&tv, v, rows, D, 128);
     if (prot) {
         ok = ok && make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 32) &&
-             make_map(&tvc, vc, static_cast<uint64_t>(bh) * nblk * 32, 128, 32);
+             make_map(&tvc, vc, static_cast<uint64_t>(bh) * nblk * 128, 64, 128);
     } else {
         tkc = tq;
         tvc = tq;
@@ -193,6 +193,8 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     p.fired = fired;
     p.fired_cap = fired ? fired_cap : 0;
     p.observe_linear = d->observe_linear;
+    p.exp_lo = std::isfinite(d->eps1) ? static_cast<float>(std::exp(-d->eps1)) : 0.0f;
+    p.exp_hi = std::isfinite(d->eps1) ? static_cast<float>(std::exp(d->eps1)) : INFINITY;
     const bool dbg = d->debug != 0;
     cudaError_t e = (D == 64) ? efta_launch_attn_d64(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st)
                               : efta_launch_attn_d128(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);

@@ -5,8 +5,9 @@
 //   KC[32 x D]   row x     : c1_hi  of  sum_l K[j*128 + x + 8l][:]         (x < 8)
 //                row 8+x   : c2_hi  of  sum_l (l+1) K[j*128 + x + 8l][:]
 //                row 16+x  : c1_lo, row 24+x: c2_lo
-//   VC[32 x 128] row x     : c1_hi of sum_g V[j*128 + key][x + 8g]  (column = key)
-//                ... same row order
+//   VC[128 x 64] row = key : cols x / 8+x / 16+x / 24+x = c1_hi / c2_hi / c1_lo / c2_lo
+//                of sum_g V[j*128 + key][x + 8g]; cols 32..63 zero (MN-major operand
+//                appended to V_j, see efta_attn.cuh)
 // c1/c2 follow encode_strided (src/abft.cpp:19-42): unit and (l+1) group
 // weights, fp32 accumulation in ascending l. K's checksums run over the key
 // (column) index of K_j^T = the score tile's columns; V's run over head_dim =
@@ -53,9 +54,10 @@ __global__ void __launch_bounds__(256) efta_encode_kv_kernel(const __half* __res
         kc[(crow0 + 24 + x) * D + dim] = __float2half_rn(__fsub_rn(c2, __half2float(h2)));
     }
     __syncthreads();
-    // VC: one thread per (x, key)
+    // VC (MN-major, one 64-wide row per key): thread per (key, x)
+    const size_t vrow0 = (static_cast<size_t>(head) * nblk + j) * 128;
     for (int t = threadIdx.x; t < 8 * 128; t += blockDim.x) {
-        const int x = t / 128, key = t % 128;
+        const int key = t / 8, x = t % 8;
         float c1 = 0.0f, c2 = 0.0f;
 #pragma unroll
         for (int g = 0; g < G_O; ++g) {
@@ -64,10 +66,15 @@ __global__ void __launch_bounds__(256) efta_encode_kv_kernel(const __half* __res
             c2 = __fadd_rn(c2, __fmul_rn(static_cast<float>(g + 1), val));
         }
         const __half h1 = __float2half_rn(c1), h2 = __float2half_rn(c2);
-        vc[(crow0 + x) * 128 + key] = h1;
-        vc[(crow0 + 8 + x) * 128 + key] = h2;
-        vc[(crow0 + 16 + x) * 128 + key] = __float2half_rn(__fsub_rn(c1, __half2float(h1)));
-        vc[(crow0 + 24 + x) * 128 + key] = __float2half_rn(__fsub_rn(c2, __half2float(h2)));
+        __half* dst = vc + (vrow0 + key) * 64;
+        dst[x] = h1;
+        dst[8 + x] = h2;
+        dst[16 + x] = __float2half_rn(__fsub_rn(c1, __half2float(h1)));
+        dst[24 + x] = __float2half_rn(__fsub_rn(c2, __half2float(h2)));
+        dst[32 + x] = __float2half_rn(0.0f);
+        dst[40 + x] = __float2half_rn(0.0f);
+        dst[48 + x] = __float2half_rn(0.0f);
+        dst[56 + x] = __float2half_rn(0.0f);
     }
 }
 
