@@ -1,0 +1,262 @@
+"""CPU: pin the oracle restatement (oracle/efta_oracle.c).
+
+1. Known-answer tests restated from the reference's own unit tests
+   (/root/reference/proj/tests/test_*.cpp, cited per test).
+2. Golden fixtures produced by the unmodified reference (tests/golden/, made by
+   tests/golden/make_golden.py from oracle/_ref).
+3. Bit-exact agreement with the compiled reference when oracle/_ref is present.
+"""
+import json
+import math
+import os
+import struct
+
+import numpy as np
+import pytest
+
+from helpers import oracle
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden")
+REF_SO = os.path.join(HERE, "..", "oracle", "_ref", "libefta_ref.so")
+
+
+def bits(x):
+    return np.asarray(x, np.float32).view(np.uint32)
+
+
+# ---------------------------------------------------------------- KATs
+def test_half_round_trip_exhaustive():  # test_core.cpp:17-30
+    orc = oracle()
+    for h in range(0, 0x10000, 7):
+        f = orc.h2f(h)
+        back = orc.f2h(f)
+        if math.isnan(f):
+            assert (back >> 10) & 0x1F == 0x1F and back & 0x3FF
+        else:
+            assert back == h
+
+
+def test_half_rounding_constants():  # test_core.cpp:32-59
+    orc = oracle()
+    q = lambda x: orc.h2f(orc.f2h(x))  # noqa: E731
+    assert q(65504.0) == 65504.0
+    assert math.isinf(q(65520.0)) and math.isinf(q(65536.0))
+    assert q(65519.0) == 65504.0
+    ulp = 2.0 ** -10
+    assert q(1.0 + 2 ** -12) == 1.0
+    assert q(1.0 + 3 * 2 ** -12) == 1.0 + ulp
+    assert q(1.0 + 2 ** -11) == 1.0
+    assert q(1.0 + 3 * 2 ** -11) == 1.0 + 2 * ulp
+    assert orc.h2f(0x0001) == 2.0 ** -24
+    assert q(2.0 ** -25) == 0.0
+    assert q(1.5 * 2 ** -25) == 2.0 ** -24
+    assert orc.f2h(-0.0) == 0x8000
+
+
+def test_flip_bit_kats():  # test_fault.cpp:26-31
+    orc = oracle()
+    assert orc.flip_bit(1.0, 32, 31) == -1.0
+    assert math.isinf(orc.flip_bit(1.0, 32, 30))
+    assert orc.flip_bit(1.0, 32, 22) == 1.5
+    assert orc.flip_bit(1.0, 32, 23) == 0.5
+    nz = orc.flip_bit(0.0, 32, 31)
+    assert nz == 0.0 and math.copysign(1.0, nz) < 0
+    assert orc.flip_bit(1.0, 16, 15) == -1.0
+    assert orc.flip_bit(1.0, 16, 10) == 0.5
+
+
+def test_encode_strided_ones():  # test_abft.cpp:12-22
+    c1, c2 = oracle().encode_strided(np.ones((1, 16), np.float32), 8)
+    assert (c1 == 2.0).all() and (c2 == 3.0).all()
+
+
+def test_single_error_located_and_repaired():  # test_abft.cpp:24-40
+    orc = oracle()
+    t = orc.random_matrix(301, 3, 16, half=False)
+    orig = t.copy()
+    c1, c2 = orc.encode_strided(t, 8)
+    t[2, 13] += 1.0
+    rep = orc.verify_locate_correct(t, c1, c2, 1e-4)
+    assert rep["status"] == "corrected" and (rep["row"], rep["col"]) == (2, 13)
+    assert rep["corrections"] == 1 and rep["violations"] == 1
+    assert abs(rep["residual"] - 1.0) < 1e-3
+    assert np.abs(t - orig).max() < 1e-5
+
+
+def test_two_errors_one_column_not_mended():  # test_abft.cpp:53-66
+    orc = oracle()
+    t = orc.random_matrix(311, 1, 16, half=False)
+    orig = t.copy()
+    c1, c2 = orc.encode_strided(t, 8)
+    t[0, 3] += 1.0
+    t[0, 11] += 0.5
+    rep = orc.verify_locate_correct(t, c1, c2, 1e-4)
+    assert rep["status"] == "detected_uncorrectable"
+    assert np.abs(t - orig).max() > 0.4
+
+
+def test_two_errors_distinct_columns_repaired():  # test_abft.cpp:68-80
+    orc = oracle()
+    t = orc.random_matrix(313, 2, 16, half=False)
+    orig = t.copy()
+    c1, c2 = orc.encode_strided(t, 8)
+    t[1, 3] += 1.0
+    t[1, 12] -= 0.5
+    rep = orc.verify_locate_correct(t, c1, c2, 1e-4)
+    assert rep["status"] == "corrected" and rep["corrections"] == 2
+    assert np.abs(t - orig).max() < 1e-5
+
+
+def test_nan_cell_restored():  # test_abft.cpp:96-107
+    orc = oracle()
+    t = orc.random_matrix(317, 2, 16, half=False)
+    orig = t.copy()
+    c1, c2 = orc.encode_strided(t, 8)
+    t[1, 5] = np.nan
+    rep = orc.verify_locate_correct(t, c1, c2, 1e-4)
+    assert rep["status"] == "corrected"
+    assert np.abs(t - orig).max() < 1e-5
+
+
+def test_checksummed_gemm_propagation():  # test_abft.cpp:119-134, 154-166
+    orc = oracle()
+    a = orc.random_matrix(331, 8, 12)
+    bt = orc.random_matrix(332, 12, 16)
+    c, c1, c2 = orc.checksummed_gemm(a, bt, 8)
+    d1, d2 = orc.encode_strided(c, 8)
+    assert np.abs(c1 - d1).max() < 1e-5 and np.abs(c2 - d2).max() < 1e-4
+    clean = c.copy()
+    c[5, 6] -= 0.25
+    rep = orc.verify_locate_correct(c, c1, c2, 1e-4)
+    assert rep["status"] == "corrected" and (rep["row"], rep["col"]) == (5, 6)
+    assert np.abs(c - clean).max() < 1e-5
+
+
+def test_two_error_enumeration():  # acceptance.cpp:215-258 (check 5)
+    orc = oracle()
+    base = orc.random_matrix(0x2E22, 1, 64, half=False)
+    c1, c2 = orc.encode_strided(base, 8)
+    mismatch = 0
+    for a in range(64):
+        for b in range(a + 1, 64):
+            t = base.copy()
+            t[0, a] += 1.0
+            t[0, b] += 0.5
+            orc.verify_locate_correct(t, c1, c2, 1e-4)
+            fixed = np.abs(t - base).max() < 1e-4
+            mismatch += fixed != ((a % 8) != (b % 8))
+    assert mismatch == 0
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_protected_modes_bit_identical(seed):  # test_efta.cpp:28-46
+    orc = oracle()
+    q, k, v, _ = orc.gen_trial(seed, 64, 32, 16, 8)
+    base = orc.efta_forward(q, k, v, 16, 8, mode="none")
+    for mode in ("efta", "efta-opt"):
+        r = orc.efta_forward(q, k, v, 16, 8, mode=mode, thr=(7e-6, 0.48, 0.48))
+        assert np.array_equal(bits(r.o), bits(base.o))
+        assert r.detections == 0 and not r.failed
+
+
+def test_check_cadence():  # test_efta.cpp:48-70
+    orc = oracle()
+    q, k, v, _ = orc.gen_trial(42, 64, 32, 16, 8)
+    full = orc.efta_forward(q, k, v, 16, 8, mode="efta")
+    opt = orc.efta_forward(q, k, v, 16, 8, mode="efta-opt")
+    assert full.summary.exp_checks == 16 and opt.summary.exp_checks == 16
+    assert full.summary.output_checks == 20 and opt.summary.output_checks == 4
+    finals = [e for e in opt.events if e["kind"] == "output_checksum"]
+    assert len(finals) == 4 and all(e["block_j"] == 4 for e in finals)
+
+
+def test_overhead_identity():  # test_efta.cpp:72-90, acceptance.cpp:351-362
+    orc = oracle()
+    q, k, v, _ = orc.gen_trial(77, 128, 64, 32, 8)
+    s = orc.efta_forward(q, k, v, 32, 8, mode="efta-opt").summary
+    assert s.flops_cs_gemm_scores * 32 == s.flops_main_gemm_scores * 16
+    assert s.flops_cs_gemm_output * 64 == s.flops_main_gemm_output * 16
+
+
+@pytest.mark.parametrize("spec,expect", [
+    ("GEMM1_OUT:1:2:3:4:30", "corrected"), ("SUB_MAX:0:1:5:6:31", None),
+    ("EXP_OUT:2:1:7:8:31", "bitexact"), ("REDUCE_MAX:1:1:2:0:30", None),
+    ("REDUCE_MAX:1:2:2:0:29", "factor"), ("REDUCE_SUM:0:3:4:0:30", "range"),
+    ("RESCALE_FACTOR:3:1:2:9:31", None), ("GEMM2_ACC:2:2:8:10:30", None),
+    ("NORMALIZE_OUT:1:0:3:12:22", None)])
+def test_single_fault_kats(spec, expect):  # test_efta.cpp:92-174
+    orc = oracle()
+    q, k, v, _ = orc.gen_trial(99, 64, 32, 16, 8)
+    thr = (7e-6, 1e-4, 1e-4)
+    ref = orc.efta_forward(q, k, v, 16, 8, mode="efta-opt", thr=thr)
+    r = orc.efta_forward(q, k, v, 16, 8, mode="efta-opt", thr=thr, specs=[spec])
+    assert not r.failed
+    if expect == "range":
+        assert r.range_replacements > 0
+        assert np.argmax(r.o[4]) == np.argmax(ref.o[4])
+        return
+    assert r.detections > 0
+    if expect == "bitexact":
+        assert r.recomputes > 0 and np.array_equal(bits(r.o), bits(ref.o))
+    elif expect == "factor":
+        assert any(e["kind"] == "factor_range" and e["status"] != "clean" for e in r.events)
+    tol = 1e-4 if expect in ("corrected", "factor") or spec.startswith(("SUB", "REDUCE_MAX")) else 1e-2
+    assert np.abs(r.o - ref.o).max() < tol
+
+
+def test_flash_matches_standard():  # acceptance.cpp:65-84 (check 1), reduced
+    orc = oracle()
+    for n, d, b in [(64, 32, 16), (256, 64, 64)]:
+        for s in range(3):
+            q, k, v, _ = orc.gen_trial(orc.trial_seed(1000 + n + d + b, s), n, d, b, 8)
+            of = orc.efta_forward(q, k, v, b, 8, mode="none").o
+            os_ = orc.standard_attention(q, k, v, b, 8)
+            assert np.abs(of - os_).max() <= 1e-3
+
+
+# ---------------------------------------------------------------- golden fixtures
+def _index():
+    with open(os.path.join(GOLD, "index.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("name", sorted(_index()))
+def test_oracle_matches_reference_golden(name):
+    meta = _index()[name]
+    g = np.load(os.path.join(GOLD, f"{name}.npz"))
+    orc = oracle()
+    q, k, v, _ = orc.gen_trial(int(g["seed"]), meta["seq"], meta["d"], meta["block"], meta["stride"])
+    r = orc.efta_forward(q, k, v, meta["block"], meta["stride"], mode=meta["mode"],
+                         thr=tuple(meta["thr"]), specs=meta["specs"])
+    assert np.array_equal(bits(r.o), bits(g["o"])), "O differs bitwise from the reference"
+    assert np.array_equal(bits(r.m), bits(g["m"])) and np.array_equal(bits(r.l), bits(g["l"]))
+    kinds = ["score_checksum", "exp_checksum", "factor_range", "rowsum_range", "output_checksum"]
+    stat = ["clean", "corrected", "detected_uncorrectable", "nonfinite"]
+    ev = np.array([[kinds.index(e["kind"]), e["block_i"], e["block_j"], stat.index(e["status"]),
+                    e["row"], e["col"], e["violations"], e["corrections"]] for e in r.events],
+                  np.int32).reshape(-1, 8)
+    assert np.array_equal(ev, g["events"])
+    assert list(g["summary"]) == [r.detections, r.corrections, r.recomputes,
+                                  r.range_replacements, int(r.failed)]
+
+
+# ---------------------------------------------------------------- vs compiled reference
+@pytest.mark.skipif(not os.path.exists(REF_SO), reason="oracle/_ref not built")
+def test_oracle_bit_exact_vs_reference_random_campaign():
+    from oracle import Oracle
+    ref, port = Oracle("ref"), oracle()
+    for t in range(40):
+        seed = ref.trial_seed(7, t)
+        q, k, v, spec = ref.gen_trial(seed, 128, 64, 32, 8, sites=list(range(8)))
+        q2, k2, v2, spec2 = port.gen_trial(seed, 128, 64, 32, 8, sites=list(range(8)))
+        assert spec == spec2 and np.array_equal(q, q2)
+        for mode in ("efta", "efta-opt"):
+            a = ref.efta_forward(q, k, v, 32, 8, mode=mode, thr=(7e-6, 1e-4, 1e-4), specs=[spec])
+            b = port.efta_forward(q, k, v, 32, 8, mode=mode, thr=(7e-6, 1e-4, 1e-4), specs=[spec])
+            assert np.array_equal(bits(a.o), bits(b.o))
+            assert [(e["kind"], e["block_i"], e["block_j"], e["status"], e["row"], e["col"])
+                    for e in a.events] == [(e["kind"], e["block_i"], e["block_j"], e["status"],
+                                            e["row"], e["col"]) for e in b.events]
+            assert (a.detections, a.corrections, a.recomputes, a.failed) == \
+                   (b.detections, b.corrections, b.recomputes, b.failed)
