@@ -79,6 +79,31 @@ int efta_attn_encode_kv_f16(const efta_attn_desc* d, const uint16_t* k, const ui
 
 float efta_flip_bit(float v, int width, int bit);
 
+/* ---- strided-ABFT GEMM (feed-forward linear layers) ----
+ * Y[m x n] = X[m x k] . W^T with W stored [n x k] (nn.Linear layout), fp16 in / fp32
+ * accumulate / fp16 out. Every 256-wide output column tile carries strided checksums
+ * (stride 8, 32 groups) computed on the tensor cores from the weight's precomputed
+ * checksum rows and verified / located / corrected per output row in the epilogue.
+ * Faults (debug=1 only): efta_fault_spec with block_i = global row, col = global col,
+ * bit = bit to flip in that fp32 accumulator value before verification. Events are
+ * reported with kind EFTA_BLOCK_CHECKSUM, head = n-tile, block_i = m-tile, global row/col. */
+typedef struct {
+    int m, n, k;
+    int stride;  /* 8 */
+    int n_tile;  /* 256 */
+    double eps;  /* absolute threshold of verify_locate_correct (abft.hpp:58-60) */
+    int debug;
+} efta_gemm_desc;
+
+size_t efta_abft_weight_cs_bytes(const efta_gemm_desc* d);
+/* wcs: [n/256 * 32, k] fp16 = hi/lo split strided checksums of each weight tile */
+int efta_abft_encode_weight_f16(const efta_gemm_desc* d, const uint16_t* w, uint16_t* wcs,
+                                void* stream);
+int efta_abft_gemm_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w,
+                       const uint16_t* wcs, uint16_t* y, const efta_fault_spec* faults,
+                       int n_faults, efta_event* events, int ev_cap, efta_counters* counters,
+                       void* stream);
+
 /* ---- host-side helpers of the reference campaign (host memory only) ---- */
 /* trial_seed (include/efta/rng.hpp:55-58) */
 uint64_t efta_trial_seed(uint64_t base, uint64_t trial);

@@ -1,0 +1,402 @@
+// abft_gemm.cu — strided-ABFT tcgen05 GEMM for the feed-forward layers (sm_100a).
+//
+// Y[M x N] = X[M x K] . W^T, W stored [N x K] (nn.Linear layout, K-major), fp16 in,
+// fp32 accumulate in TMEM, fp16 out. Replaces the reference's checksummed_gemm +
+// verify_locate_correct (src/abft.cpp:322-369, :65-187) applied per 256-wide output
+// column tile: for every output row r of a tile and checksum
+// column x in [0, 8):
+//     c1[r][x] = sum_l Y[r][x + 8l],  c2[r][x] = sum_l (l+1) Y[r][x + 8l],  l < 32
+// computed by the tensor cores from the weight's strided checksum rows
+// (Wc = encode_strided over the tile's output columns, hi/lo fp16 split,
+// precomputed once per weight) and verified in the epilogue by the thread that owns
+// row r (TMEM lane r) — no shuffles, no shared-memory reductions.
+//
+// Tile: 128 x 256 (+32 checksum cols). Each k-step issues two N=144 MMAs:
+//   [W rows 0..127  | Wc_hi rows 0..15] -> TMEM cols [0, 144)
+//   [W rows 128..255| Wc_lo rows 0..15] -> TMEM cols [144, 288)
+// so A is read twice per k-step and the checksum work is 32/256 = 12.5% extra MMA.
+// Persistent grid (one CTA per SM), static round-robin tile order (m-major rows of
+// n-tiles so consecutive CTAs share X rows in L2).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+
+#include "../../include/efta_b200.h"
+#include "efta_attn.cuh"
+#include "efta_launch.h"
+
+using namespace efta_sm100;
+
+namespace {
+
+constexpr int GM = 128, GN = 256, GK = 64;   // tile and k-chunk
+constexpr int STAGES = 4;
+constexpr uint32_t A_BYTES = GM * GK * 2;            // 16 KB
+constexpr uint32_t B_HALF = (128 + 16) * GK * 2;     // 18 KB: 128 W rows + 16 checksum rows
+constexpr uint32_t B_BYTES = 2 * B_HALF;             // 36 KB
+constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+constexpr uint32_t OFF_BAR = STAGES * STAGE;
+constexpr uint32_t OFF_TMEM = OFF_BAR + (2 * STAGES + 2) * 8;
+constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
+constexpr uint32_t SMEM_BYTES = OFF_RED + 128 * 24 + 256 + 1024;
+
+struct GemmParams {
+    int m, n, k, m_tiles, n_tiles, k_chunks;
+    double eps;
+    __half* y;
+    const efta_fault_spec* faults;  // site ignored; block_i = global row, col = global col
+    int n_faults;
+    efta_event* events;
+    int ev_cap;
+    efta_counters* counters;
+};
+
+struct RowScratchG {
+    RowSlot* slots;
+    int* ints;
+    double* dbl;
+};
+
+template <bool DBG>
+__global__ void __launch_bounds__(256, 1)
+abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                 const __grid_constant__ CUtensorMap tm_wc, const GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+    const int warp = warp_id(), lane = lane_id();
+    const int n_tiles_total = p.m_tiles * p.n_tiles;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 128);
+        fence_barrier_init();
+        tma_prefetch_desc(&tm_x);
+        tma_prefetch_desc(&tm_w);
+        tma_prefetch_desc(&tm_wc);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ------------------------------------------ TMA producer
+            int it = 0;
+            for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+                const int mt = t / p.n_tiles, nt = t % p.n_tiles;
+                for (int kc = 0; kc < p.k_chunks; ++kc, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    uint8_t* a = smem + s * STAGE;
+                    uint8_t* b = a + A_BYTES;
+                    mbar_arrive_expect_tx(&full[s], STAGE);
+                    tma_load_2d(a, &tm_x, &full[s], kc * GK, mt * GM, kEvictNormal);
+                    tma_load_2d(b, &tm_w, &full[s], kc * GK, nt * GN, kEvictLast);
+                    tma_load_2d(b + 16384, &tm_wc, &full[s], kc * GK, nt * 32, kEvictLast);
+                    tma_load_2d(b + B_HALF, &tm_w, &full[s], kc * GK, nt * GN + 128, kEvictLast);
+                    tma_load_2d(b + B_HALF + 16384, &tm_wc, &full[s], kc * GK, nt * 32 + 16, kEvictLast);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ------------------------------------------ MMA issuer
+            constexpr uint32_t ID = idesc_f16_f32(128, 144, 0, 0);
+            const uint32_t sbase = smem_u32(smem);
+            int it = 0, tl = 0;
+            for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
+                mbar_wait(tempty, (tl & 1) ^ 1);  // epilogue drained the accumulator
+                tc_fence_after();
+                for (int kc = 0; kc < p.k_chunks; ++kc, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t a = sbase + s * STAGE, b = a + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < GK / 16; ++kk) {
+                        const uint64_t ad = smem_desc_sw128(a + kk * 32, 16, 1024);
+                        const uint32_t acc = (kc | kk) > 0;
+                        mma_ss(tmem, ad, smem_desc_sw128(b + kk * 32, 16, 1024), ID, acc);
+                        mma_ss(tmem + 144, ad, smem_desc_sw128(b + B_HALF + kk * 32, 16, 1024), ID, acc);
+                    }
+                    tc_commit(&empty[s]);
+                }
+                tc_commit(tfull);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ------------------------------------------------------- epilogue (thread = row)
+        const int wq = warp - 4, row = wq * 32 + lane;
+        const uint32_t lb = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+        RowScratchG rs;
+        rs.slots = reinterpret_cast<RowSlot*>(smem + OFF_RED);
+        rs.ints = reinterpret_cast<int*>(smem + OFF_RED + 128 * sizeof(RowSlot));
+        rs.dbl = reinterpret_cast<double*>(smem + OFF_RED + 128 * sizeof(RowSlot) + 16 * sizeof(int));
+        float fam = 0.0f;
+        int tl = 0;
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
+            const int mt = t / p.n_tiles, nt = t % p.n_tiles;
+            const int grow = mt * GM + row;
+            // this row's injected upset, if any (global coordinates)
+            int f_col = -1, f_bit = 0;
+            if (DBG)
+                for (int i = 0; i < p.n_faults; ++i)
+                    if (p.faults[i].block_i == grow && p.faults[i].col / GN == nt) {
+                        f_col = p.faults[i].col % GN;
+                        f_bit = p.faults[i].bit;
+                    }
+            mbar_wait(tfull, tl & 1);
+            tc_fence_after();
+            float s1[8], s2[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) { s1[x] = 0.0f; s2[x] = 0.0f; }
+            __half* yrow = p.y + static_cast<size_t>(grow) * p.n + nt * GN;
+            bool nonfin = false;
+#pragma unroll 1
+            for (int c = 0; c < 8; ++c) {
+                float v[32];
+                tmem_ld32(lb + (c < 4 ? c * 32 : 144 + (c - 4) * 32), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                tmem_wait_ld();
+                if (DBG && f_col >= c * 32 && f_col < c * 32 + 32) {
+#pragma unroll
+                    for (int x = 0; x < 32; ++x)
+                        if (x == f_col - c * 32) v[x] = __uint_as_float(__float_as_uint(v[x]) ^ (1u << f_bit));
+                }
+#pragma unroll
+                for (int l4 = 0; l4 < 4; ++l4) {
+                    const float w = static_cast<float>(c * 4 + l4 + 1);
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) {
+                        const float val = v[l4 * 8 + x];
+                        s1[x] = __fadd_rn(s1[x], val);
+                        s2[x] = __fadd_rn(s2[x], __fmul_rn(w, val));
+                        nonfin |= !isfinite(val);
+                    }
+                }
+                uint4 pk[4];
+                uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+                for (int x = 0; x < 16; ++x) pw[x] = pack_half2(v[2 * x], v[2 * x + 1]);
+                uint4* dst = reinterpret_cast<uint4*>(yrow + c * 32);
+#pragma unroll
+                for (int x = 0; x < 4; ++x) dst[x] = pk[x];
+            }
+            uint32_t hi[16], lo[16];
+            tmem_ld16(lb + 128, hi);
+            tmem_ld16(lb + 272, lo);
+            tmem_wait_ld();
+            float c1[8], c2[8];
+            bool viol = nonfin, cs_bad = false;
+            double res = 0.0;
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                c1[x] = __fadd_rn(__uint_as_float(hi[x]), __uint_as_float(lo[x]));
+                c2[x] = __fadd_rn(__uint_as_float(hi[8 + x]), __uint_as_float(lo[8 + x]));
+                cs_bad |= !isfinite(c1[x]) || !isfinite(c2[x]);
+                const double d1 = static_cast<double>(c1[x]) - s1[x];
+                const double d2 = static_cast<double>(c2[x]) - s2[x];
+                if (!isfinite(d1) || !isfinite(d2)) { viol = true; continue; }
+                res = fmax(res, fmax(fabs(d1), fabs(d2) / 32.0));
+                viol |= fabs(d1) > p.eps || fabs(d2) > p.eps * 32.0;
+            }
+            fam = fmaxf(fam, static_cast<float>(res));
+            const bool tile_cs_bad = named_bar_or(4, 128, cs_bad);
+            if (named_bar_or(5, 128, viol || cs_bad)) {
+                // locate / correct from the still-resident accumulator row
+                RowVerify rv{};
+                rv.best_col = -1;
+                rv.restored_col = -1;
+                rv.residual = res;
+                const bool need = !tile_cs_bad && viol;
+                if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld is warp-collective
+                    float tloc[GN];
+                    for (int c = 0; c < 8; ++c) {
+                        uint32_t r32[32];
+                        tmem_ld32(lb + (c < 4 ? c * 32 : 144 + (c - 4) * 32), r32);
+                        tmem_wait_ld();
+                        for (int x = 0; x < 32; ++x) tloc[c * 32 + x] = __uint_as_float(r32[x]);
+                    }
+                    if (need) {
+                        if (DBG && f_col >= 0)
+                            tloc[f_col] = __uint_as_float(__float_as_uint(tloc[f_col]) ^ (1u << f_bit));
+                        float before[GN];
+                        for (int c = 0; c < GN; ++c) before[c] = tloc[c];
+                        verify_row<GN>(tloc, c1, c2, p.eps, rv);
+                        for (int c = 0; c < GN; ++c)
+                            if (__float_as_uint(tloc[c]) != __float_as_uint(before[c]))
+                                yrow[c] = __float2half_rn(tloc[c]);
+                    }
+                }
+                TileReport tr = reduce_tile_report(rv, tile_cs_bad, row, rs.slots, rs.ints, rs.dbl);
+                if (row == 0 && tr.status != EFTA_CLEAN) {
+                    efta_counters* cn = p.counters;
+                    atomicAdd(&cn->detections, 1);
+                    atomicAdd(&cn->corrections, tr.corrections);
+                    if (tr.status == EFTA_DETECTED_UNCORRECTABLE || tr.status == EFTA_NONFINITE)
+                        atomicExch(&cn->failed, 1);
+                    const int slot = atomicAdd(&cn->n_events, 1);
+                    if (slot < p.ev_cap) {
+                        efta_event& e = p.events[slot];
+                        e.kind = EFTA_BLOCK_CHECKSUM;
+                        e.head = nt;
+                        e.block_i = mt;
+                        e.block_j = 0;
+                        e.status = tr.status;
+                        e.row = tr.row >= 0 ? mt * GM + tr.row : -1;
+                        e.col = tr.col >= 0 ? nt * GN + tr.col : -1;
+                        e.violations = tr.violations;
+                        e.corrections = tr.corrections;
+                        e.checksum_repair = tr.checksum_repair;
+                        e.residual = tr.residual;
+                        e.delta = tr.delta;
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) fam = fmaxf(fam, __shfl_xor_sync(0xffffffffu, fam, off));
+        if (lane == 0) atomic_max_nonneg(&p.counters->family_max[1], fam);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// weight checksum rows: Wc[t][32][K] from W[N][K] over each 256-wide output tile
+__global__ void __launch_bounds__(256) encode_weight_kernel(const __half* __restrict__ w,
+                                                            __half* __restrict__ wc, int n, int k) {
+    const int t = blockIdx.y;
+    const int kk = blockIdx.x * blockDim.x + threadIdx.x;
+    if (kk >= k) return;
+#pragma unroll 1
+    for (int x = 0; x < 8; ++x) {
+        float c1 = 0.0f, c2 = 0.0f;
+        for (int l = 0; l < GN / 8; ++l) {
+            const float v = __half2float(w[static_cast<size_t>(t * GN + x + 8 * l) * k + kk]);
+            c1 = __fadd_rn(c1, v);
+            c2 = __fadd_rn(c2, __fmul_rn(static_cast<float>(l + 1), v));
+        }
+        const __half h1 = __float2half_rn(c1), h2 = __float2half_rn(c2);
+        const size_t r0 = static_cast<size_t>(t) * 32;
+        wc[(r0 + x) * k + kk] = h1;
+        wc[(r0 + 8 + x) * k + kk] = h2;
+        wc[(r0 + 16 + x) * k + kk] = __float2half_rn(__fsub_rn(c1, __half2float(h1)));
+        wc[(r0 + 24 + x) * k + kk] = __float2half_rn(__fsub_rn(c2, __half2float(h2)));
+    }
+}
+
+int gfail(int code, const std::string& m) {
+    efta_internal_set_error(m.c_str());
+    return code;
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool gmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int gvalidate(const efta_gemm_desc* d) {
+    if (!d) return gfail(1, "abft_gemm: null descriptor");
+    if (d->m <= 0 || d->n <= 0 || d->k <= 0) return gfail(1, "abft_gemm: dimensions must be positive");
+    if (d->stride != 8) return gfail(1, "abft_gemm: stride must be 8");
+    if (d->n_tile != GN) return gfail(1, "abft_gemm: n_tile must be 256");
+    if (d->m % GM) return gfail(1, "abft_gemm: m must be a multiple of 128");
+    if (d->n % GN) return gfail(1, "abft_gemm: n must be a multiple of 256");
+    if (d->k % GK) return gfail(1, "abft_gemm: k must be a multiple of 64");
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t efta_abft_weight_cs_bytes(const efta_gemm_desc* d) {
+    if (gvalidate(d)) return 0;
+    return static_cast<size_t>(d->n / GN) * 32 * d->k * sizeof(__half);
+}
+
+int efta_abft_encode_weight_f16(const efta_gemm_desc* d, const uint16_t* w, uint16_t* wcs,
+                                void* stream) {
+    if (int rc = gvalidate(d)) return rc;
+    dim3 grid((d->k + 255) / 256, d->n / GN);
+    encode_weight_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const __half*>(w), reinterpret_cast<__half*>(wcs), d->n, d->k);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : gfail(2, cudaGetErrorString(e));
+}
+
+int efta_abft_gemm_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w,
+                       const uint16_t* wcs, uint16_t* y, const efta_fault_spec* faults, int n_faults,
+                       efta_event* events, int ev_cap, efta_counters* counters, void* stream) {
+    if (int rc = gvalidate(d)) return rc;
+    if (!x || !w || !wcs || !y || !counters) return gfail(1, "abft_gemm: null buffer");
+    if (n_faults > 0 && !d->debug) return gfail(1, "abft_gemm: fault injection needs debug=1");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(efta_counters), st);
+    if (e != cudaSuccess) return gfail(2, cudaGetErrorString(e));
+    CUtensorMap tx, tw, twc;
+    if (!gmap(&tx, x, d->m, d->k, 128) || !gmap(&tw, w, d->n, d->k, 128) ||
+        !gmap(&twc, wcs, static_cast<uint64_t>(d->n / GN) * 32, d->k, 16))
+        return gfail(2, "abft_gemm: cuTensorMapEncodeTiled failed");
+    GemmParams p{};
+    p.m = d->m;
+    p.n = d->n;
+    p.k = d->k;
+    p.m_tiles = d->m / GM;
+    p.n_tiles = d->n / GN;
+    p.k_chunks = d->k / GK;
+    p.eps = d->eps;
+    p.y = reinterpret_cast<__half*>(y);
+    p.faults = faults;
+    p.n_faults = faults ? n_faults : 0;
+    p.events = events;
+    p.ev_cap = events ? ev_cap : 0;
+    p.counters = counters;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = p.m_tiles * p.n_tiles;
+    const int grid = tiles < nsm ? tiles : nsm;
+    auto launch = [&](auto kern) -> cudaError_t {
+        cudaError_t ee = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        if (ee != cudaSuccess) return ee;
+        kern<<<grid, 256, SMEM_BYTES, st>>>(tx, tw, twc, p);
+        return cudaGetLastError();
+    };
+    e = d->debug ? launch(abft_gemm_kernel<true>) : launch(abft_gemm_kernel<false>);
+    return e == cudaSuccess ? 0 : gfail(2, cudaGetErrorString(e));
+}
+
+}  // extern "C"

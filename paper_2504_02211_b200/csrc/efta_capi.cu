@@ -111,6 +111,8 @@ int encode_kv(const efta_attn_desc* d, const void* k, const void* v, void* kc, v
 
 }  // namespace
 
+void efta_internal_set_error(const char* msg) { g_err = msg; }
+
 extern "C" {
 
 const char* efta_last_error(void) { return g_err.c_str(); }

@@ -14,3 +14,6 @@ cudaError_t efta_launch_attn_d128(int mode, bool dbg, const CUtensorMap& tq, con
                                   const CUtensorMap& tv, const CUtensorMap& tkc,
                                   const CUtensorMap& tvc, const efta_sm100::AttnParams& p, int bh,
                                   cudaStream_t st);
+
+// shared thread-local error string behind efta_last_error()
+void efta_internal_set_error(const char* msg);

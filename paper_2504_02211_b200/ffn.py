@@ -1,0 +1,102 @@
+"""Strided-ABFT linear layers for the feed-forward block (FT-Transformer, arXiv 2504.02211).
+
+    lin = AbftLinear(weight)        # weight: CUDA fp16 [out_features, in_features]
+    y, rep = lin(x)                 # x: CUDA fp16 [tokens, in_features] -> y fp16
+
+Mirrors the reference's checksummed_gemm + verify_locate_correct (reference
+include/efta/abft.hpp:58-77) applied to every 256-wide output column tile; the
+weight's strided checksum rows are encoded once at construction (weights are
+static). The compute is libefta_b200.so's tcgen05 kernel (csrc/abft_gemm.cu).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .attention import FTReport, KINDS, STATUS
+
+_EXPORTS = ("efta_abft_gemm_f16", "efta_abft_encode_weight_f16", "efta_abft_weight_cs_bytes")
+for _n in _EXPORTS:
+    if not hasattr(lib, _n):
+        raise ImportError(f"libefta_b200.so lacks {_n}: rebuild the library")
+
+
+class AbftLinear:
+    def __init__(self, weight: torch.Tensor, eps: float = 1e-2, debug: bool = False,
+                 ev_cap: int = 4096):
+        if weight.dtype != torch.float16 or not weight.is_cuda or weight.dim() != 2:
+            raise _lib.ConfigError("AbftLinear: weight must be a 2-D CUDA fp16 tensor [N, K]")
+        self.weight = weight.contiguous()
+        self.n, self.k = self.weight.shape
+        self.eps = eps
+        self.debug = debug
+        desc = _lib.GemmDesc(128, self.n, self.k, 8, 256, eps, 1 if debug else 0)
+        check(_validate(desc))
+        nbytes = lib.efta_abft_weight_cs_bytes(C.byref(desc))
+        self.wcs = torch.empty(nbytes // 2, dtype=torch.float16, device=weight.device)
+        check(lib.efta_abft_encode_weight_f16(C.byref(desc), self.weight.data_ptr(),
+                                              self.wcs.data_ptr(),
+                                              torch.cuda.current_stream(weight.device).cuda_stream))
+        dev = weight.device
+        self.counters = torch.zeros(C.sizeof(_lib.Counters), dtype=torch.uint8, device=dev)
+        self.ev_cap = ev_cap
+        self.events = torch.zeros(ev_cap * C.sizeof(_lib.Event), dtype=torch.uint8, device=dev)
+        self.faults = None
+        self.n_faults = 0
+
+    def set_faults(self, faults):
+        """faults: iterable of (row, col, bit) in global output coordinates."""
+        faults = list(faults or [])
+        self.n_faults = len(faults)
+        if not faults:
+            self.faults = None
+            return
+        arr = (_lib.FaultSpec * len(faults))(
+            *[_lib.FaultSpec(0, 0, r, 0, 0, c, b, 1) for (r, c, b) in faults])
+        self.faults = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(self.weight.device)
+
+    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None):
+        if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[1] != self.k:
+            raise _lib.ConfigError("AbftLinear: x must be CUDA fp16 [tokens, in_features]")
+        x = x.contiguous()
+        m = x.shape[0]
+        if y is None:
+            y = torch.empty((m, self.n), dtype=torch.float16, device=x.device)
+        desc = _lib.GemmDesc(m, self.n, self.k, 8, 256, self.eps, 1 if self.debug else 0)
+        check(lib.efta_abft_gemm_f16(
+            C.byref(desc), x.data_ptr(), self.weight.data_ptr(), self.wcs.data_ptr(), y.data_ptr(),
+            self.faults.data_ptr() if self.faults is not None else None, self.n_faults,
+            self.events.data_ptr(), self.ev_cap, self.counters.data_ptr(),
+            torch.cuda.current_stream(x.device).cuda_stream))
+        return y
+
+    def report(self) -> FTReport:
+        cnt = _lib.Counters.from_buffer_copy(bytes(self.counters.cpu().numpy()))
+        rep = FTReport(mode="abft", detections=cnt.detections, corrections=cnt.corrections,
+                       failed=bool(cnt.failed), family_max=tuple(cnt.family_max))
+        ne = min(cnt.n_events, self.ev_cap)
+        if ne:
+            raw = bytes(self.events[: ne * C.sizeof(_lib.Event)].cpu().numpy())
+            for i in range(ne):
+                e = _lib.Event.from_buffer_copy(raw, i * C.sizeof(_lib.Event))
+                rep.events.append(dict(kind=KINDS[e.kind], n_tile=e.head, m_tile=e.block_i,
+                                       status=STATUS[e.status], row=e.row, col=e.col,
+                                       violations=e.violations, corrections=e.corrections,
+                                       checksum_repair=e.checksum_repair, residual=e.residual,
+                                       delta=e.delta))
+        return rep
+
+
+def _validate(desc) -> int:
+    # efta_abft_weight_cs_bytes returns 0 on an invalid descriptor and sets the error
+    return 0 if lib.efta_abft_weight_cs_bytes(C.byref(desc)) else 1
+
+
+def abft_gemm(x: torch.Tensor, weight: torch.Tensor, eps: float = 1e-2):
+    """One-shot protected linear: returns (y, FTReport)."""
+    lin = AbftLinear(weight, eps=eps)
+    y = lin(x)
+    return y, lin.report()
