@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libefta_b200.so")
+LIB_PATH = os.environ.get("EFTA_LIB") or os.path.join(PKG, "libefta_b200.so")
 
 SITES = ["GEMM1_OUT", "SUB_MAX", "EXP_OUT", "REDUCE_MAX", "REDUCE_SUM",
          "RESCALE_FACTOR", "GEMM2_ACC", "NORMALIZE_OUT"]

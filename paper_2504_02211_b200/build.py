@@ -11,12 +11,17 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libefta_b200.so")
+BUILD = os.path.join(PKG, "_build_prof" if os.environ.get("EFTA_PROF") == "1" else
+                     (f"_build_{os.environ['EFTA_VARIANT']}" if os.environ.get("EFTA_VARIANT") else "_build"))
+PROF = os.environ.get("EFTA_PROF") == "1"   # phase-timestamp build (tools/phase_prof.py)
+VARIANT = os.environ.get("EFTA_VARIANT", "")  # experiment builds: extra -D flags, separate .so
+LIB = os.path.join(PKG, "libefta_b200_prof.so" if PROF else
+                   (f"libefta_b200_{VARIANT}.so" if VARIANT else "libefta_b200.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-         "--expt-relaxed-constexpr"]
+         "--expt-relaxed-constexpr"] + (["-DEFTA_PROF"] if os.environ.get("EFTA_PROF") == "1" else []) + \
+        os.environ.get("EFTA_DEFS", "").split()
 
 # translation units: (source, extra defines) — the attention instantiations are
 # split per head dim so they compile in parallel

@@ -1,6 +1,7 @@
 // efta_attn_inst.cu — instantiations of the fused attention kernel for one head
 // dim (EFTA_INST_D), all modes x {fast, debug/tap} variants.
 #include "efta_attn_kernel.cuh"
+#include "efta_attn_pair.cuh"
 #include "efta_launch.h"
 
 #ifndef EFTA_INST_D
@@ -25,7 +26,7 @@ cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtenso
         attr_set = true;
     }
     dim3 grid(p.nblk, bh);
-    kern<<<grid, 256, L::SMEM_BYTES, st>>>(tq, tk, tv, tkc, tvc, p);
+    kern<<<grid, attn_threads(MODE, DBG), L::SMEM_BYTES, st>>>(tq, tk, tv, tkc, tvc, p);
     return cudaGetLastError();
 }
 
@@ -43,6 +44,23 @@ cudaError_t launch_d(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMa
     }
 }
 
+template <int D, int MODE>
+cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const CUtensorMap& tkb,
+                          const CUtensorMap& tkc, const CUtensorMap& tvt, const AttnParams& p, int bh,
+                          cudaStream_t st) {
+    using PL = PairLayout<D, MODE != 0>;
+    auto kern = efta_attn_pair_kernel<D, MODE>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    dim3 grid(p.nblk, bh);
+    kern<<<grid, 256, PL::SMEM_BYTES, st>>>(tq, tka, tkb, tkc, tvt, p);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 #if EFTA_INST_D == 64
@@ -58,5 +76,43 @@ cudaError_t efta_launch_attn_d128(int mode, bool dbg, const CUtensorMap& tq, con
                                   const CUtensorMap& tvc, const AttnParams& p, int bh,
                                   cudaStream_t st) {
     return launch_d<128>(mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
+}
+#endif
+
+#if EFTA_INST_D == 64
+cudaError_t efta_launch_attn_pair_d64(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
+                                      const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
+                                      const AttnParams& p, int bh, cudaStream_t st) {
+    return mode == 0 ? launch_pair_t<64, 0>(tq, tka, tkb, tkc, tvt, p, bh, st)
+                     : launch_pair_t<64, 2>(tq, tka, tkb, tkc, tvt, p, bh, st);
+}
+cudaError_t efta_launch_encode_pair_d64(bool prot, const void* k, const void* v, void* kc, void* vt,
+                                        int seq_len, int nblk, int bh, cudaStream_t st) {
+    dim3 grid(nblk, bh);
+    if (prot)
+        efta_encode_pair_kernel<64, true><<<grid, 256, 0, st>>>(static_cast<const __half*>(k), static_cast<const __half*>(v),
+                                                             static_cast<__half*>(kc), static_cast<__half*>(vt), seq_len, nblk);
+    else
+        efta_encode_pair_kernel<64, false><<<grid, 256, 0, st>>>(static_cast<const __half*>(k), static_cast<const __half*>(v),
+                                                              static_cast<__half*>(kc), static_cast<__half*>(vt), seq_len, nblk);
+    return cudaGetLastError();
+}
+#else
+cudaError_t efta_launch_attn_pair_d128(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
+                                       const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
+                                       const AttnParams& p, int bh, cudaStream_t st) {
+    return mode == 0 ? launch_pair_t<128, 0>(tq, tka, tkb, tkc, tvt, p, bh, st)
+                     : launch_pair_t<128, 2>(tq, tka, tkb, tkc, tvt, p, bh, st);
+}
+cudaError_t efta_launch_encode_pair_d128(bool prot, const void* k, const void* v, void* kc, void* vt,
+                                         int seq_len, int nblk, int bh, cudaStream_t st) {
+    dim3 grid(nblk, bh);
+    if (prot)
+        efta_encode_pair_kernel<128, true><<<grid, 256, 0, st>>>(static_cast<const __half*>(k), static_cast<const __half*>(v),
+                                                              static_cast<__half*>(kc), static_cast<__half*>(vt), seq_len, nblk);
+    else
+        efta_encode_pair_kernel<128, false><<<grid, 256, 0, st>>>(static_cast<const __half*>(k), static_cast<const __half*>(v),
+                                                               static_cast<__half*>(kc), static_cast<__half*>(vt), seq_len, nblk);
+    return cudaGetLastError();
 }
 #endif

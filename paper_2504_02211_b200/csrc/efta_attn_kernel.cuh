@@ -111,7 +111,7 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                     // same formula as the fast path so untouched cells reproduce their bits;
                     // a linearly repaired cell only exists in the scaled domain
                     e = (__fmul_rn(raw[c], p.scale) == sc[c])
-                            ? ex2_approx(fmaf(raw[c], scale_log2, -mL))
+                            ? ex2_col(c, fmaf(raw[c], scale_log2, -mL))
                             : ex2_approx(__fsub_rn(sc[c], mm) * kLog2e);
                 }
                 if (__float_as_uint(e) != __float_as_uint(p_loc[c])) changed = 1;
@@ -200,7 +200,7 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                     e = tap(p, EFTA_EXP_OUT, j, c, e);
                 } else {
                     e = (__fmul_rn(raw[c], p.scale) == sc[c])
-                            ? ex2_approx(fmaf(raw[c], scale_log2, -mL))
+                            ? ex2_col(c, fmaf(raw[c], scale_log2, -mL))
                             : ex2_approx(__fsub_rn(sc[c], mm) * kLog2e);
                 }
                 p_loc[c] = e;
@@ -285,14 +285,476 @@ __device__ __forceinline__ void verify_output_tile(const AttnParams& p, float (&
                    tr.corrections, tr.checksum_repair, tr.residual, tr.delta);
 }
 
+}  // namespace efta_sm100
+
+#include "efta_attn_split.cuh"
+
+namespace efta_sm100 {
+
+
+template <bool PAIR>
+__device__ __forceinline__ void signal_p_ready(uint64_t* bar, int lane) {
+    if constexpr (PAIR) {
+        // one arrival per warp on the pair leader's barrier (its MMA reads both CTAs' P)
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(bar, 0);
+    } else {
+        mbar_arrive(bar);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Row warpgroup (warps 4..7, thread t = query row t = TMEM lane t): softmax, exp-stage
+// check, factor guard, O correction, epilogue. Shared by the single-CTA kernel and the
+// CTA-pair (cta_group::2) kernel; only the P-ready signal differs.
+template <int D, int MODE, bool DBG, bool PAIR>
+__device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64_t* s_full,
+                                       uint64_t* p_ready, uint64_t* o_done, uint32_t tmem, int warp,
+                                       int lane, int head, int qt, int n, int seq_row0) {
+    using L = AttnLayout<D>;
+    constexpr bool PROT = MODE != EFTA_MODE_NONE;
+    constexpr bool LAZY = attn_lazy(MODE, DBG);
+    const int wq = warp - 4;
+    const int row = wq * 32 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    RowScratch rs;
+    rs.slots = reinterpret_cast<RowSlot*>(red);
+    rs.ints = reinterpret_cast<int*>(red + 128 * sizeof(RowSlot));
+    rs.dbl = reinterpret_cast<double*>(red + 128 * sizeof(RowSlot) + 16 * sizeof(int));
+
+    ThreadTap tap{};
+    if (DBG) {
+        for (int i = 0; i < p.n_faults; ++i) {
+            const efta_fault_spec f = p.faults[i];
+            if (f.head == head && f.block_i == qt && f.row == row) {
+                tap.active = 1;
+                tap.site = f.site;
+                tap.bj = f.block_j;
+                tap.col = f.col;
+                tap.bit = f.bit;
+                tap.trigger = f.trigger;
+                tap.count = 0;
+                tap.idx = i;
+            }
+        }
+    }
+    const float scale = p.scale, scale_log2 = p.scale_log2;
+    // m_run: the max P is referenced to (== the running max unless LAZY);
+    // m_true: the running row max (the reference's m) when rescaling lazily
+    float m_run = -CUDART_INF_F, l_run = 0.0f, lb = 0.0f, m_true = -CUDART_INF_F;
+    float fam_exp = 0.0f, fam_lin = 0.0f, fam_out = 0.0f;
+
+    for (int j = 0; j < n; ++j) {
+        const int b = j & 1;
+        const uint32_t s_addr = lane_base + L::COL_S0 + b * L::S_STRIDE;
+        const uint32_t cs_addr = s_addr + 128;  // 16 hi + 16 lo checksum product cols
+        if (warp == 4) EFTA_TS(0, j);
+        mbar_wait(&s_full[b], (j >> 1) & 1);
+        if (warp == 4) EFTA_TS(1, j);
+        tc_fence_after();
+        float pv[kBlock];
+        uint32_t csr[16], csl[16];
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4)
+            tmem_ld32(s_addr + c4 * 32, *reinterpret_cast<uint32_t(*)[32]>(&pv[c4 * 32]));
+        if (PROT) {
+            tmem_ld16(cs_addr, csr);
+            tmem_ld16(cs_addr + 16, csl);
+        }
+        tmem_wait_ld();
+        if (PROT) {
+#pragma unroll
+            for (int x = 0; x < 16; ++x)
+                csr[x] = __float_as_uint(__fadd_rn(__uint_as_float(csr[x]), __uint_as_float(csl[x])));
+        }
+
+        float bm, m_new;
+        const float m_true_before = m_true;
+        int sc_fault_col = -1;
+        float sc_fault_val = 0.0f;
+        if (DBG) {
+            // explicit reference sequence so every named site can be tapped
+#pragma unroll
+            for (int c = 0; c < kBlock; ++c) {
+                const float sc0 = __fmul_rn(pv[c], scale);
+                const float sc1 = tap(p, EFTA_GEMM1_OUT, j, c, sc0);
+                if (__float_as_uint(sc1) != __float_as_uint(sc0)) { sc_fault_col = c; sc_fault_val = sc1; }
+                pv[c] = sc1;
+            }
+            if (PROT && p.observe_linear) {
+                // efta.cpp:181-185: linear score check every iteration with eps = inf
+                // (observation only); residual = max(|d1|, |d2|/G) (abft.cpp:135)
+                float lin = 0.0f;
+#pragma unroll
+                for (int x = 0; x < kStride; ++x) {
+                    float a = 0.0f, bb = 0.0f;
+#pragma unroll
+                    for (int l = 0; l < kBlock / kStride; ++l) {
+                        a = __fadd_rn(a, pv[x + kStride * l]);
+                        bb = __fadd_rn(bb, __fmul_rn(static_cast<float>(l + 1), pv[x + kStride * l]));
+                    }
+                    const float d1 = fabsf(__fmul_rn(__uint_as_float(csr[x]), scale) - a);
+                    const float d2 = fabsf(__fmul_rn(__uint_as_float(csr[kStride + x]), scale) - bb) /
+                                     static_cast<float>(kBlock / kStride);
+                    lin = fmaxf(lin, fmaxf(d1, d2));
+                }
+                if (isfinite(lin)) fam_lin = fmaxf(fam_lin, lin);
+            }
+            bm = pv[0];
+#pragma unroll
+            for (int c = 1; c < kBlock; ++c) bm = (bm < pv[c]) ? pv[c] : bm;
+            bm = bm + p.rowmax_bias;
+            m_new = (m_run < bm) ? bm : m_run;
+            m_new = tap(p, EFTA_REDUCE_MAX, j, 0, m_new);
+#pragma unroll
+            for (int c = 0; c < kBlock; ++c) {
+                float a = __fsub_rn(pv[c], m_new);
+                a = tap(p, EFTA_SUB_MAX, j, c, a);
+                float e = ex2_approx(a * kLog2e);
+                pv[c] = tap(p, EFTA_EXP_OUT, j, c, e);
+            }
+        } else {
+            float mx0 = pv[0], mx1 = pv[1], mx2 = pv[2], mx3 = pv[3];
+#pragma unroll
+            for (int c = 4; c < kBlock; c += 4) {
+                mx0 = fmaxf(mx0, pv[c]);
+                mx1 = fmaxf(mx1, pv[c + 1]);
+                mx2 = fmaxf(mx2, pv[c + 2]);
+                mx3 = fmaxf(mx3, pv[c + 3]);
+            }
+            bm = __fmul_rn(fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)), scale) + p.rowmax_bias;
+            if (LAZY) {
+                m_true = (m_true < bm) ? bm : m_true;
+                m_new = (j == 0 || m_true - m_run > kLazyTau) ? m_true : m_run;
+            } else {
+                m_new = (m_run < bm) ? bm : m_run;
+            }
+            const float mL = m_new * kLog2e;
+            const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
+#pragma unroll
+            for (int c = 0; c < kBlock; c += 2) {
+                const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
+                if (exp_on_fma(c)) {
+                    const float2 e = ex2_poly2(a);
+                    pv[c] = e.x;
+                    pv[c + 1] = e.y;
+                } else {
+                    pv[c] = ex2_approx(a.x);
+                    pv[c + 1] = ex2_approx(a.y);
+                }
+            }
+        }
+
+        // ---- exp-domain strided product check (SNVR; snvr.cpp:52-83):
+        // group x: prod_l P[x + 8l] vs Pc1 = exp(scale*c1 - 16 m); the reference's
+        // log-domain test |sum log P - log Pc1| > eps1 becomes the bracket
+        // prod outside [Pc1 e^-eps1, Pc1 e^eps1] (no log on the fast path).
+        const float f = ex2_approx((m_run - m_new) * kLog2e);
+        bool exp_affected = false, factor_bad = false;
+        float exp_res = 0.0f;
+        int exp_viol = 0;
+        if (PROT) {
+            float2 prod[kStride / 2];
+#pragma unroll
+            for (int x = 0; x < kStride / 2; ++x) prod[x] = make_float2(pv[2 * x], pv[2 * x + 1]);
+#pragma unroll
+            for (int l = 1; l < kBlock / kStride; ++l)
+#pragma unroll
+                for (int x = 0; x < kStride / 2; ++x)
+                    prod[x] = fmul2(prod[x], make_float2(pv[kStride * l + 2 * x], pv[kStride * l + 2 * x + 1]));
+            const float g16m = 16.0f * m_new;
+            bool degenerate = !isfinite(m_new);
+#pragma unroll
+            for (int x = 0; x < kStride; ++x) {
+                const float pr = (x & 1) ? prod[x >> 1].y : prod[x >> 1].x;
+                const float c1s = __fmul_rn(__uint_as_float(csr[x]), scale);
+                const float pc1 = ex2_approx(__fsub_rn(c1s, g16m) * kLog2e);
+                const bool bad = !(pr >= pc1 * p.exp_lo && pr <= pc1 * p.exp_hi);
+                if (DBG) {
+                    if (!(pr > 0.0f && pr < CUDART_INF_F) || !(pc1 > 0.0f && pc1 < CUDART_INF_F)) {
+                        degenerate = true;
+                    } else {
+                        const float d = fabsf(lg2_approx(__fdividef(pr, pc1))) * kLn2;
+                        exp_res = fmaxf(exp_res, d);
+                    }
+                }
+                if (bad) { exp_affected = true; ++exp_viol; }
+            }
+            if (degenerate) { exp_affected = true; exp_res = CUDART_INF_F; exp_viol = 1; }
+            if (j > 0) factor_bad = !(f > 0.0f && f <= 1.0f);  // NaN fails both
+            if (DBG && isfinite(exp_res)) fam_exp = fmaxf(fam_exp, exp_res);
+            if (named_bar_or(6, 128, exp_affected || factor_bad)) {
+                float p_loc[kBlock];
+#pragma unroll
+                for (int c = 0; c < kBlock; ++c) p_loc[c] = pv[c];
+                int replaced = 0;
+                const float m_true_prev = m_true_before;
+                exp_stage_slow<DBG>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res,
+                                    exp_viol, m_run, m_new, bm, p_loc, replaced, tap, sc_fault_col,
+                                    sc_fault_val, rs);
+                if (replaced) {
+#pragma unroll
+                    for (int c = 0; c < kBlock; ++c) pv[c] = p_loc[c];
+                }
+                // the recovered reference max is the row's true max so far
+                if (LAZY) m_true = (m_true_prev < m_new) ? m_new : m_true_prev;
+            }
+        }
+
+        if (warp == 4) EFTA_TS(2, j);
+        // ---- rescale factor, lower bound, denominator (efta.cpp:192-242)
+        const float fr = PROT ? ex2_approx((m_run - m_new) * kLog2e) : f;  // m_new may be repaired
+        if (PROT) lb = __fadd_rn(__fmul_rn(lb, fr), ex2_approx((bm - m_new) * kLog2e));
+        float2 ps0 = make_float2(pv[0], pv[1]), ps1 = make_float2(pv[2], pv[3]);
+#pragma unroll
+        for (int c = 4; c < kBlock; c += 4) {
+            ps0 = fadd2(ps0, make_float2(pv[c], pv[c + 1]));
+            ps1 = fadd2(ps1, make_float2(pv[c + 2], pv[c + 3]));
+        }
+        l_run = __fadd_rn(__fmul_rn(fr, l_run), (ps0.x + ps0.y) + (ps1.x + ps1.y));
+        if (DBG) l_run = tap(p, EFTA_REDUCE_SUM, j, 0, l_run);
+
+        if (warp == 4) EFTA_TS(3, j);
+        // ---- P (fp16) over the S columns it came from
+        {
+            uint32_t pk[32];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int x = 0; x < 32; ++x) pk[x] = pack_half2(pv[h * 64 + 2 * x], pv[h * 64 + 2 * x + 1]);
+                tmem_st32(s_addr + h * 32, pk);
+            }
+        }
+
+        // ---- O correction: O *= f (and its checksum columns)
+        if (j > 0) {
+            if (warp == 4) EFTA_TS(4, j);
+            mbar_wait(o_done, (j - 1) & 1);
+            if (warp == 4) EFTA_TS(5, j);
+            tc_fence_after();
+            if (MODE == EFTA_MODE_EFTA) {
+                // per-iteration output check of the accumulator after GEMM II of j-1
+                float o[D];
+                uint32_t oc[32];
+#pragma unroll
+                for (int c = 0; c < D / 32; ++c)
+                    tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
+                tmem_ld32(lane_base + L::COL_O + D, oc);
+                tmem_wait_ld();
+#pragma unroll
+                for (int x = 0; x < 16; ++x) {
+                    oc[x] = __float_as_uint(__fadd_rn(__uint_as_float(oc[x]), __uint_as_float(oc[16 + x])));
+                    oc[16 + x] = 0u;
+                }
+                if (DBG) {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) o[c] = tap(p, EFTA_GEMM2_ACC, j - 1, c, o[c]);
+                }
+                float c1[kStride], c2[kStride];
+#pragma unroll
+                for (int x = 0; x < kStride; ++x) { c1[x] = __uint_as_float(oc[x]); c2[x] = __uint_as_float(oc[kStride + x]); }
+                float res;
+                verify_output_tile<D>(p, o, c1, c2, p.eps2, head, qt, j - 1, row, rs, res);
+                if (isfinite(res)) fam_out = fmaxf(fam_out, res);
+#pragma unroll
+                for (int c = 0; c < D; ++c) o[c] = __fmul_rn(o[c], fr);
+                if (DBG) {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) o[c] = tap(p, EFTA_RESCALE_FACTOR, j, c, o[c]);
+                }
+#pragma unroll
+                for (int x = 0; x < kStride; ++x) { oc[x] = __float_as_uint(__fmul_rn(c1[x], fr)); oc[kStride + x] = __float_as_uint(__fmul_rn(c2[x], fr)); }
+#pragma unroll
+                for (int c = 0; c < D / 32; ++c)
+                    tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
+                tmem_st32(lane_base + L::COL_O + D, oc);
+            } else {
+                const bool need = DBG || !__all_sync(0xffffffffu, fr == 1.0f);
+                if (need && DBG) {
+#pragma unroll
+                    for (int c = 0; c < D / 32; ++c) {
+                        float o[32];
+                        tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int x = 0; x < 32; ++x) {
+                            float v = tap(p, EFTA_GEMM2_ACC, j - 1, c * 32 + x, o[x]);
+                            v = __fmul_rn(v, fr);
+                            o[x] = tap(p, EFTA_RESCALE_FACTOR, j, c * 32 + x, v);
+                        }
+                        tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+                    }
+                }
+                if (need) {
+                    // all chunks in flight at once (P's registers are free by now)
+                    constexpr int NCH = DBG ? (PROT ? 1 : 0) : (D / 32 + (PROT ? 1 : 0));
+                    constexpr int C0 = DBG ? D / 32 : 0;
+                    float o[NCH > 0 ? NCH : 1][32];
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+                        tmem_ld32(lane_base + L::COL_O + (C0 + c) * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
+                    tmem_wait_ld();
+                    const float2 f2 = make_float2(fr, fr);
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                        for (int x = 0; x < 32; x += 2) {
+                            const float2 r2 = fmul2(make_float2(o[c][x], o[c][x + 1]), f2);
+                            o[c][x] = r2.x;
+                            o[c][x + 1] = r2.y;
+                        }
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+                        tmem_st32(lane_base + L::COL_O + (C0 + c) * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
+                }
+            }
+        } else if (DBG) {
+            // reference: oacc starts at 0 and is rescaled (0*0) + tapped at j = 0
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                float o[32];
+#pragma unroll
+                for (int x = 0; x < 32; ++x) o[x] = tap(p, EFTA_RESCALE_FACTOR, 0, c * 32 + x, 0.0f);
+                tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+            }
+            uint32_t z[32];
+#pragma unroll
+            for (int x = 0; x < 32; ++x) z[x] = 0u;
+            tmem_st32(lane_base + L::COL_O + D, z);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        signal_p_ready<PAIR>(p_ready, lane);
+        if (warp == 4) EFTA_TS(6, j);
+        m_run = m_new;
+    }
+
+    // ------------------------------------------------ epilogue
+    mbar_wait(o_done, (n - 1) & 1);
+    tc_fence_after();
+    float o[D];
+    float c1[kStride], c2[kStride];
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c)
+        tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
+    {
+        uint32_t oc[32];
+        if (PROT) tmem_ld32(lane_base + L::COL_O + D, oc);
+        tmem_wait_ld();
+#pragma unroll
+        for (int x = 0; x < kStride; ++x) {
+            c1[x] = PROT ? __fadd_rn(__uint_as_float(oc[x]), __uint_as_float(oc[16 + x])) : 0.0f;
+            c2[x] = PROT ? __fadd_rn(__uint_as_float(oc[kStride + x]), __uint_as_float(oc[16 + kStride + x]))
+                         : 0.0f;
+        }
+    }
+    if (DBG) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) o[c] = tap(p, EFTA_GEMM2_ACC, n - 1, c, o[c]);
+    }
+    if (LAZY) {
+        // bring O, its checksums, l and the lower bound from the lazy reference max to
+        // the row's true max (the reference's final m); F == 1 for most rows
+        const float F = ex2_approx((m_run - m_true) * kLog2e);
+        if (!__all_sync(0xffffffffu, F == 1.0f)) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) o[c] = __fmul_rn(o[c], F);
+#pragma unroll
+            for (int x = 0; x < kStride; ++x) { c1[x] = __fmul_rn(c1[x], F); c2[x] = __fmul_rn(c2[x], F); }
+            l_run = __fmul_rn(l_run, F);
+            lb = __fmul_rn(lb, F);
+        }
+        m_run = m_true;
+    }
+    if (MODE == EFTA_MODE_EFTA) {
+        float res;
+        verify_output_tile<D>(p, o, c1, c2, p.eps2, head, qt, n - 1, row, rs, res);
+        if (isfinite(res)) fam_out = fmaxf(fam_out, res);
+    }
+    double eps_mult = 1.0;
+    if (PROT) {
+        // denominator range restriction (snvr.cpp:161-182, efta.cpp:289-310)
+        const float upper = static_cast<float>(p.seq_len);
+        const bool bad = !isfinite(l_run) || l_run < lb || l_run > upper;
+        double viol = 0.0;
+        if (bad) {
+            viol = !isfinite(l_run) ? CUDART_INF
+                                    : (l_run < lb ? static_cast<double>(lb) - l_run
+                                                  : static_cast<double>(l_run) - upper);
+            l_run = lb;
+            eps_mult = static_cast<double>(p.seq_len) / static_cast<double>(l_run);
+        }
+        if (named_bar_or(7, 128, bad)) {
+            if (row == 0) { rs.ints[0] = 0; rs.ints[1] = 0x7fffffff; rs.dbl[0] = 0.0; }
+            wg_sync();
+            if (bad) {
+                atomicAdd(&rs.ints[0], 1);
+                atomicMin(&rs.ints[1], row);
+                unsigned long long* a = reinterpret_cast<unsigned long long*>(&rs.dbl[0]);
+                unsigned long long old = *a, assumed;
+                do {
+                    assumed = old;
+                    if (__longlong_as_double(assumed) >= viol) break;
+                    old = atomicCAS(a, assumed, __double_as_longlong(viol));
+                } while (old != assumed);
+            }
+            wg_sync();
+            if (row == 0) {
+                atomicAdd(&p.counters->range_replacements, rs.ints[0]);
+                push_event(p, EFTA_ROWSUM_RANGE, head, qt, n, EFTA_CORRECTED, rs.ints[1], -1, 0,
+                           rs.ints[0], 0, rs.dbl[0], 0.0);
+            }
+            wg_sync();
+        }
+    }
+    // normalization (efta.cpp:312-327)
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+        float v = __fdiv_rn(o[c], l_run);
+        if (DBG) v = tap(p, EFTA_NORMALIZE_OUT, 0, c, v);
+        o[c] = v;
+    }
+    if (PROT) {
+#pragma unroll
+        for (int x = 0; x < kStride; ++x) { c1[x] = __fdiv_rn(c1[x], l_run); c2[x] = __fdiv_rn(c2[x], l_run); }
+        float res;
+        verify_output_tile<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res);
+        if (isfinite(res)) fam_out = fmaxf(fam_out, res);
+    }
+    // store
+    const size_t grow = static_cast<size_t>(seq_row0) + qt * kBlock + row;
+    float4* dst = reinterpret_cast<float4*>(p.o + grow * D);
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+    if (p.m_out) p.m_out[grow] = m_run;
+    if (p.l_out) p.l_out[grow] = l_run;
+    if (PROT) {
+        // per-family worst clean residual (calibration / observation)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            fam_exp = fmaxf(fam_exp, __shfl_xor_sync(0xffffffffu, fam_exp, off));
+            fam_out = fmaxf(fam_out, __shfl_xor_sync(0xffffffffu, fam_out, off));
+            fam_lin = fmaxf(fam_lin, __shfl_xor_sync(0xffffffffu, fam_lin, off));
+        }
+        if (lane == 0) {
+            atomic_max_nonneg(&p.counters->family_max[0], fam_exp);
+            atomic_max_nonneg(&p.counters->family_max[1], fam_out);
+            if (DBG && p.observe_linear) atomic_max_nonneg(&p.counters->family_max[2], fam_lin);
+        }
+    }
+
+}
+
 // ----------------------------------------------------------------------------
 template <int D, int MODE, bool DBG>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(attn_threads(MODE, DBG), 1)
 efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
                      const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
     using L = AttnLayout<D>;
     constexpr bool PROT = MODE != EFTA_MODE_NONE;
+    constexpr bool SPLIT = attn_split(MODE, DBG);
+    constexpr bool LAZY = attn_lazy(MODE, DBG);
     constexpr int KS = L::KS, VS = L::VS, NSUB = L::NSUB;
 
     extern __shared__ uint8_t smem_raw[];
@@ -318,7 +780,7 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         for (int s = 0; s < VS; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
         mbar_init(&s_full[0], 1);
         mbar_init(&s_full[1], 1);
-        mbar_init(p_ready, 128);
+        mbar_init(p_ready, SPLIT ? 256 : 128);
         mbar_init(o_done, 1);
         fence_barrier_init();
         tma_prefetch_desc(&tm_q);
@@ -402,8 +864,11 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
             };
             issue_s(0);
             for (int j = 0; j < n; ++j) {
+                EFTA_TS(10, j);
                 if (j + 1 < n) issue_s(j + 1);
+                EFTA_TS(11, j);
                 mbar_wait(p_ready, j & 1);
+                EFTA_TS(12, j);
                 tc_fence_after();
                 const int s = j % VS;
                 mbar_wait(&v_full[s], (j / VS) & 1);
@@ -417,403 +882,20 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                            ID_PV, acc0 | (kk > 0));
                 tc_commit(&v_empty[s]);
                 tc_commit(o_done);
+                EFTA_TS(13, j);
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
-        // ------------------------------------------------ row warpgroup
-        const int wq = warp - 4;
-        const int row = wq * 32 + lane;
-        const uint32_t lane_base = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-        RowScratch rs;
-        rs.slots = reinterpret_cast<RowSlot*>(smem + L::OFF_RED);
-        rs.ints = reinterpret_cast<int*>(smem + L::OFF_RED + 128 * sizeof(RowSlot));
-        rs.dbl = reinterpret_cast<double*>(smem + L::OFF_RED + 128 * sizeof(RowSlot) + 16 * sizeof(int));
-
-        ThreadTap tap{};
-        if (DBG) {
-            for (int i = 0; i < p.n_faults; ++i) {
-                const efta_fault_spec f = p.faults[i];
-                if (f.head == head && f.block_i == qt && f.row == row) {
-                    tap.active = 1;
-                    tap.site = f.site;
-                    tap.bj = f.block_j;
-                    tap.col = f.col;
-                    tap.bit = f.bit;
-                    tap.trigger = f.trigger;
-                    tap.count = 0;
-                    tap.idx = i;
-                }
-            }
-        }
-        const float scale = p.scale, scale_log2 = p.scale_log2;
-        float m_run = -CUDART_INF_F, l_run = 0.0f, lb = 0.0f;
-        float fam_exp = 0.0f, fam_lin = 0.0f, fam_out = 0.0f;
-
-        for (int j = 0; j < n; ++j) {
-            const int b = j & 1;
-            const uint32_t s_addr = lane_base + L::COL_S0 + b * L::S_STRIDE;
-            const uint32_t cs_addr = s_addr + 128;  // 16 hi + 16 lo checksum product cols
-            mbar_wait(&s_full[b], (j >> 1) & 1);
-            tc_fence_after();
-            float pv[kBlock];
-            uint32_t csr[16], csl[16];
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4)
-                tmem_ld32(s_addr + c4 * 32, *reinterpret_cast<uint32_t(*)[32]>(&pv[c4 * 32]));
-            if (PROT) {
-                tmem_ld16(cs_addr, csr);
-                tmem_ld16(cs_addr + 16, csl);
-            }
-            tmem_wait_ld();
-            if (PROT) {
-#pragma unroll
-                for (int x = 0; x < 16; ++x)
-                    csr[x] = __float_as_uint(__fadd_rn(__uint_as_float(csr[x]), __uint_as_float(csl[x])));
-            }
-
-            float bm, m_new;
-            int sc_fault_col = -1;
-            float sc_fault_val = 0.0f;
-            if (DBG) {
-                // explicit reference sequence so every named site can be tapped
-#pragma unroll
-                for (int c = 0; c < kBlock; ++c) {
-                    const float sc0 = __fmul_rn(pv[c], scale);
-                    const float sc1 = tap(p, EFTA_GEMM1_OUT, j, c, sc0);
-                    if (__float_as_uint(sc1) != __float_as_uint(sc0)) { sc_fault_col = c; sc_fault_val = sc1; }
-                    pv[c] = sc1;
-                }
-                if (PROT && p.observe_linear) {
-                    // efta.cpp:181-185: linear score check every iteration with eps = inf
-                    // (observation only); residual = max(|d1|, |d2|/G) (abft.cpp:135)
-                    float lin = 0.0f;
-#pragma unroll
-                    for (int x = 0; x < kStride; ++x) {
-                        float a = 0.0f, bb = 0.0f;
-#pragma unroll
-                        for (int l = 0; l < kBlock / kStride; ++l) {
-                            a = __fadd_rn(a, pv[x + kStride * l]);
-                            bb = __fadd_rn(bb, __fmul_rn(static_cast<float>(l + 1), pv[x + kStride * l]));
-                        }
-                        const float d1 = fabsf(__fmul_rn(__uint_as_float(csr[x]), scale) - a);
-                        const float d2 = fabsf(__fmul_rn(__uint_as_float(csr[kStride + x]), scale) - bb) /
-                                         static_cast<float>(kBlock / kStride);
-                        lin = fmaxf(lin, fmaxf(d1, d2));
-                    }
-                    if (isfinite(lin)) fam_lin = fmaxf(fam_lin, lin);
-                }
-                bm = pv[0];
-#pragma unroll
-                for (int c = 1; c < kBlock; ++c) bm = (bm < pv[c]) ? pv[c] : bm;
-                bm = bm + p.rowmax_bias;
-                m_new = (m_run < bm) ? bm : m_run;
-                m_new = tap(p, EFTA_REDUCE_MAX, j, 0, m_new);
-#pragma unroll
-                for (int c = 0; c < kBlock; ++c) {
-                    float a = __fsub_rn(pv[c], m_new);
-                    a = tap(p, EFTA_SUB_MAX, j, c, a);
-                    float e = ex2_approx(a * kLog2e);
-                    pv[c] = tap(p, EFTA_EXP_OUT, j, c, e);
-                }
-            } else {
-                float mx0 = pv[0], mx1 = pv[1], mx2 = pv[2], mx3 = pv[3];
-#pragma unroll
-                for (int c = 4; c < kBlock; c += 4) {
-                    mx0 = fmaxf(mx0, pv[c]);
-                    mx1 = fmaxf(mx1, pv[c + 1]);
-                    mx2 = fmaxf(mx2, pv[c + 2]);
-                    mx3 = fmaxf(mx3, pv[c + 3]);
-                }
-                bm = __fmul_rn(fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)), scale) + p.rowmax_bias;
-                m_new = (m_run < bm) ? bm : m_run;
-                const float mL = m_new * kLog2e;
-                const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
-#pragma unroll
-                for (int c = 0; c < kBlock; c += 2) {
-                    const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
-                    pv[c] = ex2_approx(a.x);
-                    pv[c + 1] = ex2_approx(a.y);
-                }
-            }
-
-            // ---- exp-domain strided product check (SNVR; snvr.cpp:52-83):
-            // group x: prod_l P[x + 8l] vs Pc1 = exp(scale*c1 - 16 m); the reference's
-            // log-domain test |sum log P - log Pc1| > eps1 becomes the bracket
-            // prod outside [Pc1 e^-eps1, Pc1 e^eps1] (no log on the fast path).
-            const float f = ex2_approx((m_run - m_new) * kLog2e);
-            bool exp_affected = false, factor_bad = false;
-            float exp_res = 0.0f;
-            int exp_viol = 0;
-            if (PROT) {
-                float2 prod[kStride / 2];
-#pragma unroll
-                for (int x = 0; x < kStride / 2; ++x) prod[x] = make_float2(pv[2 * x], pv[2 * x + 1]);
-#pragma unroll
-                for (int l = 1; l < kBlock / kStride; ++l)
-#pragma unroll
-                    for (int x = 0; x < kStride / 2; ++x)
-                        prod[x] = fmul2(prod[x], make_float2(pv[kStride * l + 2 * x], pv[kStride * l + 2 * x + 1]));
-                const float g16m = 16.0f * m_new;
-                bool degenerate = !isfinite(m_new);
-#pragma unroll
-                for (int x = 0; x < kStride; ++x) {
-                    const float pr = (x & 1) ? prod[x >> 1].y : prod[x >> 1].x;
-                    const float c1s = __fmul_rn(__uint_as_float(csr[x]), scale);
-                    const float pc1 = ex2_approx(__fsub_rn(c1s, g16m) * kLog2e);
-                    const bool bad = !(pr >= pc1 * p.exp_lo && pr <= pc1 * p.exp_hi);
-                    if (DBG) {
-                        if (!(pr > 0.0f && pr < CUDART_INF_F) || !(pc1 > 0.0f && pc1 < CUDART_INF_F)) {
-                            degenerate = true;
-                        } else {
-                            const float d = fabsf(lg2_approx(__fdividef(pr, pc1))) * kLn2;
-                            exp_res = fmaxf(exp_res, d);
-                        }
-                    }
-                    if (bad) { exp_affected = true; ++exp_viol; }
-                }
-                if (degenerate) { exp_affected = true; exp_res = CUDART_INF_F; exp_viol = 1; }
-                if (j > 0) factor_bad = !(f > 0.0f && f <= 1.0f);  // NaN fails both
-                if (DBG && isfinite(exp_res)) fam_exp = fmaxf(fam_exp, exp_res);
-                if (named_bar_or(6, 128, exp_affected || factor_bad)) {
-                    float p_loc[kBlock];
-#pragma unroll
-                    for (int c = 0; c < kBlock; ++c) p_loc[c] = pv[c];
-                    int replaced = 0;
-                    exp_stage_slow<DBG>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res,
-                                        exp_viol, m_run, m_new, bm, p_loc, replaced, tap, sc_fault_col,
-                                        sc_fault_val, rs);
-                    if (replaced) {
-#pragma unroll
-                        for (int c = 0; c < kBlock; ++c) pv[c] = p_loc[c];
-                    }
-                }
-            }
-
-            // ---- rescale factor, lower bound, denominator (efta.cpp:192-242)
-            const float fr = PROT ? ex2_approx((m_run - m_new) * kLog2e) : f;  // m_new may be repaired
-            if (PROT) lb = __fadd_rn(__fmul_rn(lb, fr), ex2_approx((bm - m_new) * kLog2e));
-            float2 ps0 = make_float2(pv[0], pv[1]), ps1 = make_float2(pv[2], pv[3]);
-#pragma unroll
-            for (int c = 4; c < kBlock; c += 4) {
-                ps0 = fadd2(ps0, make_float2(pv[c], pv[c + 1]));
-                ps1 = fadd2(ps1, make_float2(pv[c + 2], pv[c + 3]));
-            }
-            l_run = __fadd_rn(__fmul_rn(fr, l_run), (ps0.x + ps0.y) + (ps1.x + ps1.y));
-            if (DBG) l_run = tap(p, EFTA_REDUCE_SUM, j, 0, l_run);
-
-            // ---- P (fp16) over the S columns it came from
-            {
-                uint32_t pk[32];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                    for (int x = 0; x < 32; ++x) pk[x] = pack_half2(pv[h * 64 + 2 * x], pv[h * 64 + 2 * x + 1]);
-                    tmem_st32(s_addr + h * 32, pk);
-                }
-            }
-
-            // ---- O correction: O *= f (and its checksum columns)
-            if (j > 0) {
-                mbar_wait(o_done, (j - 1) & 1);
-                tc_fence_after();
-                if (MODE == EFTA_MODE_EFTA) {
-                    // per-iteration output check of the accumulator after GEMM II of j-1
-                    float o[D];
-                    uint32_t oc[32];
-#pragma unroll
-                    for (int c = 0; c < D / 32; ++c)
-                        tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
-                    tmem_ld32(lane_base + L::COL_O + D, oc);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int x = 0; x < 16; ++x) {
-                        oc[x] = __float_as_uint(__fadd_rn(__uint_as_float(oc[x]), __uint_as_float(oc[16 + x])));
-                        oc[16 + x] = 0u;
-                    }
-                    if (DBG) {
-#pragma unroll
-                        for (int c = 0; c < D; ++c) o[c] = tap(p, EFTA_GEMM2_ACC, j - 1, c, o[c]);
-                    }
-                    float c1[kStride], c2[kStride];
-#pragma unroll
-                    for (int x = 0; x < kStride; ++x) { c1[x] = __uint_as_float(oc[x]); c2[x] = __uint_as_float(oc[kStride + x]); }
-                    float res;
-                    verify_output_tile<D>(p, o, c1, c2, p.eps2, head, qt, j - 1, row, rs, res);
-                    if (isfinite(res)) fam_out = fmaxf(fam_out, res);
-#pragma unroll
-                    for (int c = 0; c < D; ++c) o[c] = __fmul_rn(o[c], fr);
-                    if (DBG) {
-#pragma unroll
-                        for (int c = 0; c < D; ++c) o[c] = tap(p, EFTA_RESCALE_FACTOR, j, c, o[c]);
-                    }
-#pragma unroll
-                    for (int x = 0; x < kStride; ++x) { oc[x] = __float_as_uint(__fmul_rn(c1[x], fr)); oc[kStride + x] = __float_as_uint(__fmul_rn(c2[x], fr)); }
-#pragma unroll
-                    for (int c = 0; c < D / 32; ++c)
-                        tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
-                    tmem_st32(lane_base + L::COL_O + D, oc);
-                } else {
-                    const bool need = DBG || !__all_sync(0xffffffffu, fr == 1.0f);
-                    if (need && DBG) {
-#pragma unroll
-                        for (int c = 0; c < D / 32; ++c) {
-                            float o[32];
-                            tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int x = 0; x < 32; ++x) {
-                                float v = tap(p, EFTA_GEMM2_ACC, j - 1, c * 32 + x, o[x]);
-                                v = __fmul_rn(v, fr);
-                                o[x] = tap(p, EFTA_RESCALE_FACTOR, j, c * 32 + x, v);
-                            }
-                            tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-                        }
-                    }
-                    if (need) {
-                        // all chunks in flight at once (P's registers are free by now)
-                        constexpr int NCH = DBG ? (PROT ? 1 : 0) : (D / 32 + (PROT ? 1 : 0));
-                        constexpr int C0 = DBG ? D / 32 : 0;
-                        float o[NCH > 0 ? NCH : 1][32];
-#pragma unroll
-                        for (int c = 0; c < NCH; ++c)
-                            tmem_ld32(lane_base + L::COL_O + (C0 + c) * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
-                        tmem_wait_ld();
-                        const float2 f2 = make_float2(fr, fr);
-#pragma unroll
-                        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-                            for (int x = 0; x < 32; x += 2) {
-                                const float2 r2 = fmul2(make_float2(o[c][x], o[c][x + 1]), f2);
-                                o[c][x] = r2.x;
-                                o[c][x + 1] = r2.y;
-                            }
-#pragma unroll
-                        for (int c = 0; c < NCH; ++c)
-                            tmem_st32(lane_base + L::COL_O + (C0 + c) * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
-                    }
-                }
-            } else if (DBG) {
-                // reference: oacc starts at 0 and is rescaled (0*0) + tapped at j = 0
-#pragma unroll
-                for (int c = 0; c < D / 32; ++c) {
-                    float o[32];
-#pragma unroll
-                    for (int x = 0; x < 32; ++x) o[x] = tap(p, EFTA_RESCALE_FACTOR, 0, c * 32 + x, 0.0f);
-                    tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-                }
-                uint32_t z[32];
-#pragma unroll
-                for (int x = 0; x < 32; ++x) z[x] = 0u;
-                tmem_st32(lane_base + L::COL_O + D, z);
-            }
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(p_ready);
-            m_run = m_new;
-        }
-
-        // ------------------------------------------------ epilogue
-        mbar_wait(o_done, (n - 1) & 1);
-        tc_fence_after();
-        float o[D];
-        float c1[kStride], c2[kStride];
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c)
-            tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
-        {
-            uint32_t oc[32];
-            if (PROT) tmem_ld32(lane_base + L::COL_O + D, oc);
-            tmem_wait_ld();
-#pragma unroll
-            for (int x = 0; x < kStride; ++x) {
-                c1[x] = PROT ? __fadd_rn(__uint_as_float(oc[x]), __uint_as_float(oc[16 + x])) : 0.0f;
-                c2[x] = PROT ? __fadd_rn(__uint_as_float(oc[kStride + x]), __uint_as_float(oc[16 + kStride + x]))
-                             : 0.0f;
-            }
-        }
-        if (DBG) {
-#pragma unroll
-            for (int c = 0; c < D; ++c) o[c] = tap(p, EFTA_GEMM2_ACC, n - 1, c, o[c]);
-        }
-        if (MODE == EFTA_MODE_EFTA) {
-            float res;
-            verify_output_tile<D>(p, o, c1, c2, p.eps2, head, qt, n - 1, row, rs, res);
-            if (isfinite(res)) fam_out = fmaxf(fam_out, res);
-        }
-        double eps_mult = 1.0;
-        if (PROT) {
-            // denominator range restriction (snvr.cpp:161-182, efta.cpp:289-310)
-            const float upper = static_cast<float>(p.seq_len);
-            const bool bad = !isfinite(l_run) || l_run < lb || l_run > upper;
-            double viol = 0.0;
-            if (bad) {
-                viol = !isfinite(l_run) ? CUDART_INF
-                                        : (l_run < lb ? static_cast<double>(lb) - l_run
-                                                      : static_cast<double>(l_run) - upper);
-                l_run = lb;
-                eps_mult = static_cast<double>(p.seq_len) / static_cast<double>(l_run);
-            }
-            if (named_bar_or(7, 128, bad)) {
-                if (row == 0) { rs.ints[0] = 0; rs.ints[1] = 0x7fffffff; rs.dbl[0] = 0.0; }
-                wg_sync();
-                if (bad) {
-                    atomicAdd(&rs.ints[0], 1);
-                    atomicMin(&rs.ints[1], row);
-                    unsigned long long* a = reinterpret_cast<unsigned long long*>(&rs.dbl[0]);
-                    unsigned long long old = *a, assumed;
-                    do {
-                        assumed = old;
-                        if (__longlong_as_double(assumed) >= viol) break;
-                        old = atomicCAS(a, assumed, __double_as_longlong(viol));
-                    } while (old != assumed);
-                }
-                wg_sync();
-                if (row == 0) {
-                    atomicAdd(&p.counters->range_replacements, rs.ints[0]);
-                    push_event(p, EFTA_ROWSUM_RANGE, head, qt, n, EFTA_CORRECTED, rs.ints[1], -1, 0,
-                               rs.ints[0], 0, rs.dbl[0], 0.0);
-                }
-                wg_sync();
-            }
-        }
-        // normalization (efta.cpp:312-327)
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            float v = __fdiv_rn(o[c], l_run);
-            if (DBG) v = tap(p, EFTA_NORMALIZE_OUT, 0, c, v);
-            o[c] = v;
-        }
-        if (PROT) {
-#pragma unroll
-            for (int x = 0; x < kStride; ++x) { c1[x] = __fdiv_rn(c1[x], l_run); c2[x] = __fdiv_rn(c2[x], l_run); }
-            float res;
-            verify_output_tile<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res);
-            if (isfinite(res)) fam_out = fmaxf(fam_out, res);
-        }
-        // store
-        const size_t grow = static_cast<size_t>(seq_row0) + qt * kBlock + row;
-        float4* dst = reinterpret_cast<float4*>(p.o + grow * D);
-#pragma unroll
-        for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-        if (p.m_out) p.m_out[grow] = m_run;
-        if (p.l_out) p.l_out[grow] = l_run;
-        if (PROT) {
-            // per-family worst clean residual (calibration / observation)
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                fam_exp = fmaxf(fam_exp, __shfl_xor_sync(0xffffffffu, fam_exp, off));
-                fam_out = fmaxf(fam_out, __shfl_xor_sync(0xffffffffu, fam_out, off));
-                fam_lin = fmaxf(fam_lin, __shfl_xor_sync(0xffffffffu, fam_lin, off));
-            }
-            if (lane == 0) {
-                atomic_max_nonneg(&p.counters->family_max[0], fam_exp);
-                atomic_max_nonneg(&p.counters->family_max[1], fam_out);
-                if (DBG && p.observe_linear) atomic_max_nonneg(&p.counters->family_max[2], fam_lin);
-            }
-        }
+    } else if (SPLIT && warp >= 4) {
+        RowScratch rs2;
+        rs2.slots = reinterpret_cast<RowSlot*>(smem + L::OFF_RED);
+        rs2.ints = reinterpret_cast<int*>(smem + L::OFF_RED + 128 * sizeof(RowSlot));
+        rs2.dbl = reinterpret_cast<double*>(smem + L::OFF_RED + 128 * sizeof(RowSlot) + 16 * sizeof(int));
+        row_split<D, PROT>(p, s_full, p_ready, o_done, tmem, warp, lane, head, qt, n, seq_row0, rs2,
+                           reinterpret_cast<float*>(smem + L::OFF_XCH));
+    } else if (!SPLIT && warp >= 4) {
+        row_wg<D, MODE, DBG, false>(p, smem + L::OFF_RED, s_full, p_ready, o_done, tmem, warp, lane, head, qt, n, seq_row0);
     }
-
     tc_fence_before();
     __syncthreads();
     tc_fence_after();

@@ -6,7 +6,9 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -87,10 +89,29 @@ int validate(const efta_attn_desc* d) {
     return 0;
 }
 
-size_t ws_bytes(const efta_attn_desc* d) {
+// Workspace: [KC: bh*n*32*d fp16] [R2: max(single-CTA VC bh*n*128*64, pair V^T+VC^T
+// bh*n*(d+32)*128) fp16] [per-SM scratch rows]. All offsets 256-byte aligned.
+struct WsLayout {
+    size_t kc, r2, scratch, total;
+};
+WsLayout ws_layout(const efta_attn_desc* d) {
     const size_t bh = static_cast<size_t>(d->batch) * d->heads;
     const size_t nblk = d->seq_len / kBlock;
-    return bh * nblk * (32 * d->head_dim + 128 * 64) * sizeof(__half) + 256;
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    WsLayout w;
+    w.kc = 0;
+    w.r2 = al(bh * nblk * 32 * d->head_dim * sizeof(__half));
+    const size_t r2 = std::max(bh * nblk * 128 * 64, bh * nblk * (d->head_dim + 32) * 128) * sizeof(__half);
+    w.scratch = w.r2 + al(r2);
+    w.total = w.scratch + static_cast<size_t>(kScratchSMs) * 128 * 128 * sizeof(float);
+    return w;
+}
+size_t ws_bytes(const efta_attn_desc* d) { return ws_layout(d).total; }
+
+// the fast unprotected / EFTA-optimized variants run on CTA pairs (cta_group::2)
+bool use_pair(const efta_attn_desc* d) {
+    return !d->debug && d->mode != EFTA_MODE_EFTA && ((d->seq_len / kBlock) % 2) == 0 &&
+           std::getenv("EFTA_NO_PAIR") == nullptr;
 }
 
 int encode_kv(const efta_attn_desc* d, const void* k, const void* v, void* kc, void* vc,
@@ -112,6 +133,11 @@ int encode_kv(const efta_attn_desc* d, const void* k, const void* v, void* kc, v
 }  // namespace
 
 void efta_internal_set_error(const char* msg) { g_err = msg; }
+
+#ifdef EFTA_PROF
+static unsigned long long* efta_prof_buffer_ptr = nullptr;
+extern "C" unsigned long long* efta_prof_buffer(void) { return efta_prof_buffer_ptr; }
+#endif
 
 extern "C" {
 
@@ -152,25 +178,48 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int bh = d->batch * d->heads, nblk = d->seq_len / kBlock, D = d->head_dim;
     const bool prot = d->mode != EFTA_MODE_NONE;
-    if (prot && (workspace == nullptr || workspace_bytes < ws_bytes(d)))
+    const bool pair = use_pair(d);
+    if ((prot || pair) && (workspace == nullptr || workspace_bytes < ws_bytes(d)))
         return fail(1, "efta_attn_fwd_f16: workspace too small");
 
     CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(efta_counters), st));
-    uint16_t* kc = static_cast<uint16_t*>(workspace);
-    uint16_t* vc = kc ? kc + static_cast<size_t>(bh) * nblk * 32 * D : nullptr;
-    if (prot && !d->checksums_ready) {
-        if (int rc = encode_kv(d, k, v, kc, vc, st)) return rc;
-    }
+    const WsLayout wl = ws_layout(d);
+    char* wsb = static_cast<char*>(workspace);
+    uint16_t* kc = wsb ? reinterpret_cast<uint16_t*>(wsb + wl.kc) : nullptr;
+    uint16_t* r2 = wsb ? reinterpret_cast<uint16_t*>(wsb + wl.r2) : nullptr;
     CUtensorMap tq, tk, tv, tkc, tvc;
     const uint64_t rows = static_cast<uint64_t>(bh) * d->seq_len;
-    bool ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, rows, D, 128) &&
-              make_map(&tv, v, rows, D, 128);
-    if (prot) {
-        ok = ok && make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 32) &&
-             make_map(&tvc, vc, static_cast<uint64_t>(bh) * nblk * 128, 64, 128);
+    bool ok;
+    if (pair) {
+        // prepass: KC (protected) + [V^T ; VC^T]; then maps for the half-operands
+        if (!d->checksums_ready) {
+            cudaError_t e = D == 64 ? efta_launch_encode_pair_d64(prot, k, v, kc, r2, d->seq_len, nblk, bh, st)
+                                    : efta_launch_encode_pair_d128(prot, k, v, kc, r2, d->seq_len, nblk, bh, st);
+            if (e != cudaSuccess) return fail(2, std::string("encode: ") + cudaGetErrorString(e));
+        }
+        const int vrows = prot ? D + 32 : D;
+        ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, rows, D, prot ? 80 : 64) &&
+             make_map(&tvc, r2, static_cast<uint64_t>(bh) * nblk * vrows, 128, vrows / 2);
+        if (prot)
+            ok = ok && make_map(&tv, k, rows, D, 48) &&
+                 make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 32);
+        else {
+            tv = tk;
+            tkc = tk;
+        }
     } else {
-        tkc = tq;
-        tvc = tq;
+        if (prot && !d->checksums_ready) {
+            if (int rc = encode_kv(d, k, v, kc, r2, st)) return rc;
+        }
+        ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, rows, D, 128) &&
+             make_map(&tv, v, rows, D, 128);
+        if (prot) {
+            ok = ok && make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 32) &&
+                 make_map(&tvc, r2, static_cast<uint64_t>(bh) * nblk * 128, 64, 128);
+        } else {
+            tkc = tq;
+            tvc = tq;
+        }
     }
     if (!ok) return fail(2, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
@@ -195,11 +244,26 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     p.fired = fired;
     p.fired_cap = fired ? fired_cap : 0;
     p.observe_linear = d->observe_linear;
+    p.prof = nullptr;
+#ifdef EFTA_PROF
+    {
+        static unsigned long long* prof_buf = nullptr;
+        if (!prof_buf) cudaMalloc(&prof_buf, 64 * 32 * sizeof(unsigned long long));
+        p.prof = prof_buf;
+        efta_prof_buffer_ptr = prof_buf;
+    }
+#endif
     p.exp_lo = std::isfinite(d->eps1) ? static_cast<float>(std::exp(-d->eps1)) : 0.0f;
     p.exp_hi = std::isfinite(d->eps1) ? static_cast<float>(std::exp(d->eps1)) : INFINITY;
+    p.scratch = wsb ? reinterpret_cast<float*>(wsb + wl.scratch) : nullptr;
     const bool dbg = d->debug != 0;
-    cudaError_t e = (D == 64) ? efta_launch_attn_d64(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st)
-                              : efta_launch_attn_d128(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
+    cudaError_t e;
+    if (pair)  // maps: q, K half A, K half B (protected peer), KC, [V^T ; VC^T]
+        e = (D == 64) ? efta_launch_attn_pair_d64(d->mode, tq, tk, tv, tkc, tvc, p, bh, st)
+                      : efta_launch_attn_pair_d128(d->mode, tq, tk, tv, tkc, tvc, p, bh, st);
+    else
+        e = (D == 64) ? efta_launch_attn_d64(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st)
+                      : efta_launch_attn_d128(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
     if (e != cudaSuccess) return fail(2, std::string("attention launch: ") + cudaGetErrorString(e));
     return 0;
 }

@@ -63,7 +63,10 @@ def test_workspace_size():
     from paper_2504_02211_b200 import _lib
     d = _desc()
     ws = _lib.lib.efta_attn_workspace_bytes(C.byref(d))
-    assert ws == 12 * 4 * (32 * 64 + 128 * 64) * 2 + 256
+    al = lambda x: (x + 255) // 256 * 256  # noqa: E731
+    kc = al(12 * 4 * 32 * 64 * 2)
+    r2 = al(max(12 * 4 * 128 * 64, 12 * 4 * (64 + 32) * 128) * 2)
+    assert ws == kc + r2 + 256 * 128 * 128 * 4
 
 
 def test_python_mirror_raises_config_error():

@@ -1,0 +1,46 @@
+"""Per-phase timing of one CTA (EFTA_PROF build): EFTA_PROF=1 python -m paper_2504_02211_b200.build
+then EFTA_LIB=paper_2504_02211_b200/libefta_b200_prof.so python tools/phase_prof.py --mode none"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2504_02211_b200 import EftaAttention, Thresholds, _lib  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--mode", default="none")
+ap.add_argument("--d", type=int, default=128)
+a = ap.parse_args()
+shape = (8, 16, 8192, a.d)
+q = torch.empty(shape, device="cuda").uniform_(-1, 1).half()
+k = torch.empty(shape, device="cuda").uniform_(-1, 1).half()
+v = torch.empty(shape, device="cuda").uniform_(-1, 1).half()
+op = EftaAttention(*shape, mode=a.mode, thr=Thresholds(1e-4, 1e-3, 1e-3))
+op(q, k, v); torch.cuda.synchronize()
+op(q, k, v); torch.cuda.synchronize()
+_lib.lib.efta_prof_buffer.restype = C.c_void_p
+ptr = _lib.lib.efta_prof_buffer()
+buf = np.zeros(64 * 32, np.uint64)
+cudart = C.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libcudart.so.12") else C.CDLL("libcudart.so")
+cudart.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+cudart.cudaMemcpy(buf.ctypes.data, ptr, buf.nbytes, 2)
+t = buf.reshape(64, 32).astype(np.int64)
+names = {0: "row:wait_S", 1: "row:S_ready", 2: "row:exp_done", 3: "row:sum_done", 4: "row:P_stored",
+         5: "row:O_ready", 6: "row:p_ready", 10: "mma:iter", 11: "mma:S_issued", 12: "mma:P_ready",
+         14: "mma:V_ready", 13: "mma:PV_issued", 16: "peer:wait_S", 17: "peer:S_ready", 18: "peer:exp_done",
+         22: "peer:p_ready"}
+base = t[8, 0]
+print("iter  " + "  ".join(f"{names[s]:>13s}" for s in sorted(names)))
+for j in range(8, 16):
+    print(f"{j:4d}  " + "  ".join(f"{t[j, s] - base:13d}" for s in sorted(names)))
+print("(the clock64 counters of the two CTAs of a pair are per-SM; compare within one CTA)")
+per = np.diff(t[8:60, 0])
+print("row period median", np.median(per))
+for s_a, s_b, nm in [(0, 1, "wait S"), (1, 2, "load+max+exp"), (2, 3, "checks+sum"), (3, 4, "P pack+store"),
+                     (4, 5, "wait O(PV j-1)"), (5, 6, "correction+arrive"), (6, 0, "to next iter")]:
+    dt = [(t[j, s_b] if s_b != 0 else t[j + 1, 0]) - t[j, s_a] for j in range(8, 60)]
+    print(f"  {nm:20s} median {np.median(dt):8.0f} clk")
