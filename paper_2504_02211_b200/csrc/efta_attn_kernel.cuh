@@ -362,6 +362,7 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
             tmem_ld16(cs_addr + 16, csl);
         }
         tmem_wait_ld();
+        if (warp == 4) EFTA_TS(7, j);
         if (PROT) {
 #pragma unroll
             for (int x = 0; x < 16; ++x)
@@ -369,6 +370,9 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
         }
 
         float bm, m_new;
+        float2 prod_f[kStride / 2];   // fast path: strided group products of P
+        float pc1v[kStride];          // fast path: exp-domain checksums Pc1
+        float psum_f = 0.0f;          // fast path: row sum of P
         const float m_true_before = m_true;
         int sc_fault_col = -1;
         float sc_fault_val = 0.0f;
@@ -430,21 +434,38 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
                 m_new = (m_run < bm) ? bm : m_run;
             }
             const float mL = m_new * kLog2e;
+            if (PROT) {  // Pc1 = exp(scale*c1 - 16 m) first: these MUFUs overlap the loop below
+                const float g16m = 16.0f * m_new;
+#pragma unroll
+                for (int x = 0; x < kStride; ++x)
+                    pc1v[x] = ex2_approx(__fsub_rn(__fmul_rn(__uint_as_float(csr[x]), scale), g16m) * kLog2e);
+            }
             const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
+            float2 ps0 = make_float2(0.0f, 0.0f), ps1 = make_float2(0.0f, 0.0f);
 #pragma unroll
             for (int c = 0; c < kBlock; c += 2) {
                 const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
+                float2 e;
                 if (exp_on_fma(c)) {
-                    const float2 e = ex2_poly2(a);
-                    pv[c] = e.x;
-                    pv[c + 1] = e.y;
+                    e = ex2_poly2(a);
                 } else {
-                    pv[c] = ex2_approx(a.x);
-                    pv[c + 1] = ex2_approx(a.y);
+                    e.x = ex2_approx(a.x);
+                    e.y = ex2_approx(a.y);
+                }
+                pv[c] = e.x;
+                pv[c + 1] = e.y;
+                // row sum and the strided group products ride along (fill MUFU issue gaps)
+                if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
+                else ps0 = fadd2(ps0, e);
+                if (PROT) {
+                    const int g = (c & 7) >> 1;
+                    prod_f[g] = (c < kStride) ? e : fmul2(prod_f[g], e);
                 }
             }
+            psum_f = (ps0.x + ps0.y) + (ps1.x + ps1.y);
         }
 
+        if (warp == 4) EFTA_TS(8, j);
         // ---- exp-domain strided product check (SNVR; snvr.cpp:52-83):
         // group x: prod_l P[x + 8l] vs Pc1 = exp(scale*c1 - 16 m); the reference's
         // log-domain test |sum log P - log Pc1| > eps1 becomes the bracket
@@ -453,22 +474,28 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
         bool exp_affected = false, factor_bad = false;
         float exp_res = 0.0f;
         int exp_viol = 0;
+        bool replaced_p = false;
         if (PROT) {
             float2 prod[kStride / 2];
+            if (DBG) {
 #pragma unroll
-            for (int x = 0; x < kStride / 2; ++x) prod[x] = make_float2(pv[2 * x], pv[2 * x + 1]);
+                for (int x = 0; x < kStride / 2; ++x) prod[x] = make_float2(pv[2 * x], pv[2 * x + 1]);
 #pragma unroll
-            for (int l = 1; l < kBlock / kStride; ++l)
+                for (int l = 1; l < kBlock / kStride; ++l)
 #pragma unroll
-                for (int x = 0; x < kStride / 2; ++x)
-                    prod[x] = fmul2(prod[x], make_float2(pv[kStride * l + 2 * x], pv[kStride * l + 2 * x + 1]));
+                    for (int x = 0; x < kStride / 2; ++x)
+                        prod[x] = fmul2(prod[x], make_float2(pv[kStride * l + 2 * x], pv[kStride * l + 2 * x + 1]));
+            } else {
+#pragma unroll
+                for (int x = 0; x < kStride / 2; ++x) prod[x] = prod_f[x];
+            }
             const float g16m = 16.0f * m_new;
             bool degenerate = !isfinite(m_new);
 #pragma unroll
             for (int x = 0; x < kStride; ++x) {
                 const float pr = (x & 1) ? prod[x >> 1].y : prod[x >> 1].x;
                 const float c1s = __fmul_rn(__uint_as_float(csr[x]), scale);
-                const float pc1 = ex2_approx(__fsub_rn(c1s, g16m) * kLog2e);
+                const float pc1 = DBG ? ex2_approx(__fsub_rn(c1s, g16m) * kLog2e) : pc1v[x];
                 const bool bad = !(pr >= pc1 * p.exp_lo && pr <= pc1 * p.exp_hi);
                 if (DBG) {
                     if (!(pr > 0.0f && pr < CUDART_INF_F) || !(pc1 > 0.0f && pc1 < CUDART_INF_F)) {
@@ -483,7 +510,10 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
             if (degenerate) { exp_affected = true; exp_res = CUDART_INF_F; exp_viol = 1; }
             if (j > 0) factor_bad = !(f > 0.0f && f <= 1.0f);  // NaN fails both
             if (DBG && isfinite(exp_res)) fam_exp = fmaxf(fam_exp, exp_res);
-            if (named_bar_or(6, 128, exp_affected || factor_bad)) {
+            if (warp == 4) EFTA_TS(9, j);
+            const bool tile_trig = named_bar_or(6, 128, exp_affected || factor_bad);
+            if (warp == 4) EFTA_TS(15, j);
+            if (tile_trig) {
                 float p_loc[kBlock];
 #pragma unroll
                 for (int c = 0; c < kBlock; ++c) p_loc[c] = pv[c];
@@ -496,6 +526,7 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
 #pragma unroll
                     for (int c = 0; c < kBlock; ++c) pv[c] = p_loc[c];
                 }
+                replaced_p = replaced != 0;
                 // the recovered reference max is the row's true max so far
                 if (LAZY) m_true = (m_true_prev < m_new) ? m_new : m_true_prev;
             }
@@ -505,13 +536,17 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
         // ---- rescale factor, lower bound, denominator (efta.cpp:192-242)
         const float fr = PROT ? ex2_approx((m_run - m_new) * kLog2e) : f;  // m_new may be repaired
         if (PROT) lb = __fadd_rn(__fmul_rn(lb, fr), ex2_approx((bm - m_new) * kLog2e));
-        float2 ps0 = make_float2(pv[0], pv[1]), ps1 = make_float2(pv[2], pv[3]);
+        float psum = psum_f;
+        if (DBG || replaced_p) {  // same pairing and order as the fused sums in the exp loop
+            float2 ps0 = make_float2(pv[0], pv[1]), ps1 = make_float2(pv[2], pv[3]);
 #pragma unroll
-        for (int c = 4; c < kBlock; c += 4) {
-            ps0 = fadd2(ps0, make_float2(pv[c], pv[c + 1]));
-            ps1 = fadd2(ps1, make_float2(pv[c + 2], pv[c + 3]));
+            for (int c = 4; c < kBlock; c += 4) {
+                ps0 = fadd2(ps0, make_float2(pv[c], pv[c + 1]));
+                ps1 = fadd2(ps1, make_float2(pv[c + 2], pv[c + 3]));
+            }
+            psum = (ps0.x + ps0.y) + (ps1.x + ps1.y);
         }
-        l_run = __fadd_rn(__fmul_rn(fr, l_run), (ps0.x + ps0.y) + (ps1.x + ps1.y));
+        l_run = __fadd_rn(__fmul_rn(fr, l_run), psum);
         if (DBG) l_run = tap(p, EFTA_REDUCE_SUM, j, 0, l_run);
 
         if (warp == 4) EFTA_TS(3, j);

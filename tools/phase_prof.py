@@ -40,7 +40,8 @@ for j in range(8, 16):
 print("(the clock64 counters of the two CTAs of a pair are per-SM; compare within one CTA)")
 per = np.diff(t[8:60, 0])
 print("row period median", np.median(per))
-for s_a, s_b, nm in [(0, 1, "wait S"), (1, 2, "load+max+exp"), (2, 3, "checks+sum"), (3, 4, "P pack+store"),
+for s_a, s_b, nm in [(0, 1, "wait S"), (1, 7, "tmem load S"), (7, 8, "max+exp"), (8, 9, "product check"),
+                     (9, 15, "barrier.red.or"), (15, 2, "after or"), (2, 3, "checks+sum"), (3, 4, "P pack+store"),
                      (4, 5, "wait O(PV j-1)"), (5, 6, "correction+arrive"), (6, 0, "to next iter")]:
     dt = [(t[j, s_b] if s_b != 0 else t[j + 1, 0]) - t[j, s_a] for j in range(8, 60)]
     print(f"  {nm:20s} median {np.median(dt):8.0f} clk")
