@@ -30,7 +30,7 @@ cudart.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
 cudart.cudaMemcpy(buf.ctypes.data, ptr, buf.nbytes, 2)
 t = buf.reshape(64, 32).astype(np.int64)
 names = {0: "row:wait_S", 1: "row:S_ready", 2: "row:exp_done", 3: "row:sum_done", 4: "row:P_stored",
-         5: "row:O_ready", 6: "row:p_ready", 10: "mma:iter", 11: "mma:S_issued", 12: "mma:P_ready",
+         5: "row:O_ready", 6: "row:p_ready", 9: "mma:K_full", 10: "mma:iter", 11: "mma:S_issued", 12: "mma:P_ready",
          14: "mma:V_ready", 13: "mma:PV_issued", 16: "peer:wait_S", 17: "peer:S_ready", 18: "peer:exp_done",
          22: "peer:p_ready"}
 base = t[8, 0]
@@ -40,8 +40,9 @@ for j in range(8, 16):
 print("(the clock64 counters of the two CTAs of a pair are per-SM; compare within one CTA)")
 per = np.diff(t[8:60, 0])
 print("row period median", np.median(per))
-for s_a, s_b, nm in [(0, 1, "wait S"), (1, 7, "tmem load S"), (7, 8, "max+exp"), (8, 9, "product check"),
+for s_a, s_b, nm in [(9, 11, "S-issuer: issue S(j)"), (10, 12, "PV-issuer: wait P(j)"),
+                     (12, 14, "PV-issuer: wait V(j)"), (14, 13, "PV-issuer: issue PV(j)"), (13, 10, "PV-issuer: to next iter"), (1, 8, "split: ld+max+xchg+exp"), (8, 3, "split: checks+or+P st"), (3, 6, "split: to p_ready")] + [(0, 1, "wait S"), (1, 7, "tmem load S"), (7, 8, "max+exp"), (8, 9, "product check"),
                      (9, 15, "barrier.red.or"), (15, 2, "after or"), (2, 3, "checks+sum"), (3, 4, "P pack+store"),
                      (4, 5, "wait O(PV j-1)"), (5, 6, "correction+arrive"), (6, 0, "to next iter")]:
-    dt = [(t[j, s_b] if s_b != 0 else t[j + 1, 0]) - t[j, s_a] for j in range(8, 60)]
+    dt = [(t[j, s_b] if (s_b not in (0, 10) or s_a == 9) else t[j + 1, s_b]) - t[j, s_a] for j in range(8, 60)]
     print(f"  {nm:20s} median {np.median(dt):8.0f} clk")

@@ -9,7 +9,7 @@
 using namespace efta_sm100;
 
 template <int KIND>
-__global__ void __launch_bounds__(128, 1) kbench(float* out, int iters, unsigned long long* cyc) {
+__global__ void __launch_bounds__(512, 1) kbench(float* out, int iters, unsigned long long* cyc) {
     float2 v[8];
     for (int i = 0; i < 8; ++i) v[i] = make_float2(-0.001f * (threadIdx.x + i), -0.002f * i);
     const float2 s = make_float2(0.999f, 0.999f), b = make_float2(-0.0001f, -0.0001f);
@@ -44,14 +44,14 @@ __global__ void __launch_bounds__(128, 1) kbench(float* out, int iters, unsigned
 }
 
 template <int KIND>
-void run(const char* name, double elems_per_iter) {
+void run(const char* name, double elems_per_iter, int threads = 128) {
     float* o;
     unsigned long long* c;
-    cudaMalloc(&o, 148 * 128 * 4);
+    cudaMalloc(&o, 148 * 512 * 4);
     cudaMalloc(&c, 148 * 8);
     const int iters = 4096;
-    kbench<KIND><<<148, 128>>>(o, 16, c);
-    kbench<KIND><<<148, 128>>>(o, iters, c);
+    kbench<KIND><<<148, threads>>>(o, 16, c);
+    kbench<KIND><<<148, threads>>>(o, iters, c);
     cudaDeviceSynchronize();
     unsigned long long h[148];
     cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost);
@@ -59,7 +59,8 @@ void run(const char* name, double elems_per_iter) {
     for (int i = 0; i < 148; ++i) avg += h[i];
     avg /= 148;
     // per warp (= per SMSP here): elems_per_iter element-results per iteration
-    printf("%-34s %7.2f clk per 32-lane element batch\n", name, avg / (iters * elems_per_iter));
+    printf("%-34s warps/SMSP %d: %7.2f clk per 32-lane element batch (per SMSP)\n", name, threads / 128,
+           avg / (iters * elems_per_iter * (threads / 128)));
     cudaFree(o);
     cudaFree(c);
 }
@@ -69,5 +70,10 @@ int main() {
     run<1>("FFMA2 (2 results)", 16);
     run<2>("poly exp2 pair (2 results)", 16);
     run<3>("75% MUFU / 25% poly mix", 16);
+    run<0>("MUFU.EX2 (+FADD)", 16, 256);
+    run<2>("poly exp2 pair (2 results)", 16, 256);
+    run<3>("75% MUFU / 25% poly mix", 16, 256);
+    run<0>("MUFU.EX2 (+FADD)", 16, 512);
+    run<3>("75% MUFU / 25% poly mix", 16, 512);
     return 0;
 }
