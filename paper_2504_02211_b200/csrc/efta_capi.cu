@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/efta_b200.h"
 #include "efta_attn.cuh"
@@ -277,21 +278,41 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
                            const efta_fault_spec* faults, int n_faults, efta_event* events,
                            int ev_cap, efta_fired* fired, int fired_cap, efta_counters* counters) {
     if (int rc = validate(d)) return rc;
-    // per-thread device scratch, grown on demand and reused across calls
+    // The (batch x head) units are independent (the reference's per-head loop,
+    // src/campaign.cpp:175), so the host path streams them in chunks over three CUDA
+    // streams: H2D of chunk i+1 and D2H of chunk i-1 overlap the kernels of chunk i
+    // (separate copy engines; PCIe is full duplex). Fault-injection calls (head-indexed
+    // fault tables, fired lists) run as one chunk.
+    const int bh = d->batch * d->heads;
+    const int nchunk = (n_faults > 0 || fired) ? 1 : std::min(bh, 8);
+    const int per = (bh + nchunk - 1) / nchunk;
     struct Scratch {
         void* p = nullptr;
         size_t n = 0;
-        ~Scratch() { if (p) cudaFree(p); }
+        cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+        cudaEvent_t ev[2 * 64] = {};
+        ~Scratch() {
+            if (p) cudaFree(p);
+            for (auto& x : st) if (x) cudaStreamDestroy(x);
+            for (auto& e : ev) if (e) cudaEventDestroy(e);
+        }
     };
     thread_local Scratch s;
-    const size_t bh = static_cast<size_t>(d->batch) * d->heads;
-    const size_t n_in = bh * d->seq_len * d->head_dim;
-    const size_t bytes_in = n_in * 2, bytes_o = n_in * 4, bytes_ml = bh * d->seq_len * 4;
-    const size_t wsb = ws_bytes(d);
+    if (!s.st[0]) {
+        for (auto& x : s.st) CUDA_TRY(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        for (auto& e : s.ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const size_t head_elems = static_cast<size_t>(d->seq_len) * d->head_dim;
+    const size_t n_in = static_cast<size_t>(bh) * head_elems;
+    const size_t bytes_in = n_in * 2, bytes_o = n_in * 4, bytes_ml = static_cast<size_t>(bh) * d->seq_len * 4;
+    efta_attn_desc dc = *d;  // one chunk: batch 1 x `per` heads
+    dc.batch = 1;
+    dc.heads = per;
+    const size_t wsb = ws_bytes(&dc);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t need = 3 * al(bytes_in) + al(bytes_o) + 2 * al(bytes_ml) + al(wsb) +
-                        al(sizeof(efta_counters)) + al(sizeof(efta_fault_spec) * (n_faults + 1)) +
-                        al(sizeof(efta_event) * (ev_cap + 1)) + al(sizeof(efta_fired) * (fired_cap + 1));
+                        nchunk * al(sizeof(efta_counters)) + al(sizeof(efta_fault_spec) * (n_faults + 1)) +
+                        nchunk * al(sizeof(efta_event) * (ev_cap + 1)) + al(sizeof(efta_fired) * (fired_cap + 1));
     if (s.n < need) {
         if (s.p) cudaFree(s.p);
         s.p = nullptr;
@@ -308,31 +329,69 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
     float* dm = reinterpret_cast<float*>(take(bytes_ml));
     float* dl = reinterpret_cast<float*>(take(bytes_ml));
     void* dws = take(wsb);
-    efta_counters* dc = reinterpret_cast<efta_counters*>(take(sizeof(efta_counters)));
+    efta_counters* dcnt = reinterpret_cast<efta_counters*>(take(nchunk * al(sizeof(efta_counters))));
     efta_fault_spec* df = reinterpret_cast<efta_fault_spec*>(take(sizeof(efta_fault_spec) * (n_faults + 1)));
-    efta_event* de = reinterpret_cast<efta_event*>(take(sizeof(efta_event) * (ev_cap + 1)));
+    efta_event* de = reinterpret_cast<efta_event*>(take(nchunk * al(sizeof(efta_event) * (ev_cap + 1))));
     efta_fired* dfi = reinterpret_cast<efta_fired*>(take(sizeof(efta_fired) * (fired_cap + 1)));
-    cudaStream_t st = 0;
-    CUDA_TRY(cudaMemcpyAsync(dq, q, bytes_in, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(dk, k, bytes_in, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(dv, v, bytes_in, cudaMemcpyHostToDevice, st));
+    const size_t cnt_stride = al(sizeof(efta_counters)), ev_stride = al(sizeof(efta_event) * (ev_cap + 1));
+    cudaStream_t h2d = s.st[0], comp = s.st[1], d2h = s.st[2];
     if (n_faults > 0)
-        CUDA_TRY(cudaMemcpyAsync(df, faults, sizeof(efta_fault_spec) * n_faults, cudaMemcpyHostToDevice, st));
-    int rc = efta_attn_fwd_f16(d, dq, dk, dv, dout, dm, dl, dws, wsb, n_faults > 0 ? df : nullptr,
-                               n_faults, events ? de : nullptr, events ? ev_cap : 0,
-                               fired ? dfi : nullptr, fired ? fired_cap : 0, dc, st);
-    if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(o, dout, bytes_o, cudaMemcpyDeviceToHost, st));
-    if (m_out) CUDA_TRY(cudaMemcpyAsync(m_out, dm, bytes_ml, cudaMemcpyDeviceToHost, st));
-    if (l_out) CUDA_TRY(cudaMemcpyAsync(l_out, dl, bytes_ml, cudaMemcpyDeviceToHost, st));
-    efta_counters hc;
-    CUDA_TRY(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    if (counters) *counters = hc;
-    if (events && ev_cap > 0 && hc.n_events > 0)
-        CUDA_TRY(cudaMemcpy(events, de, sizeof(efta_event) * std::min(hc.n_events, ev_cap), cudaMemcpyDeviceToHost));
-    if (fired && fired_cap > 0 && hc.n_fired > 0)
-        CUDA_TRY(cudaMemcpy(fired, dfi, sizeof(efta_fired) * std::min(hc.n_fired, fired_cap), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpyAsync(df, faults, sizeof(efta_fault_spec) * n_faults, cudaMemcpyHostToDevice, h2d));
+    for (int c = 0; c < nchunk; ++c) {
+        const int h0 = c * per, nh = std::min(per, bh - h0);
+        if (nh <= 0) break;
+        const size_t e0 = static_cast<size_t>(h0) * head_elems, ne = static_cast<size_t>(nh) * head_elems;
+        const size_t r0 = static_cast<size_t>(h0) * d->seq_len, nr = static_cast<size_t>(nh) * d->seq_len;
+        CUDA_TRY(cudaMemcpyAsync(dq + e0, q + e0, ne * 2, cudaMemcpyHostToDevice, h2d));
+        CUDA_TRY(cudaMemcpyAsync(dk + e0, k + e0, ne * 2, cudaMemcpyHostToDevice, h2d));
+        CUDA_TRY(cudaMemcpyAsync(dv + e0, v + e0, ne * 2, cudaMemcpyHostToDevice, h2d));
+        CUDA_TRY(cudaEventRecord(s.ev[2 * c], h2d));
+        CUDA_TRY(cudaStreamWaitEvent(comp, s.ev[2 * c], 0));
+        efta_attn_desc dcc = *d;
+        if (nchunk > 1) { dcc.batch = 1; dcc.heads = nh; }
+        efta_counters* cc = reinterpret_cast<efta_counters*>(reinterpret_cast<char*>(dcnt) + c * cnt_stride);
+        efta_event* ce = reinterpret_cast<efta_event*>(reinterpret_cast<char*>(de) + c * ev_stride);
+        int rc = efta_attn_fwd_f16(&dcc, dq + e0, dk + e0, dv + e0, dout + e0, dm + r0, dl + r0, dws, wsb,
+                                   n_faults > 0 ? df : nullptr, n_faults, events ? ce : nullptr,
+                                   events ? ev_cap : 0, fired ? dfi : nullptr, fired ? fired_cap : 0, cc, comp);
+        if (rc) return rc;
+        CUDA_TRY(cudaEventRecord(s.ev[2 * c + 1], comp));
+        CUDA_TRY(cudaStreamWaitEvent(d2h, s.ev[2 * c + 1], 0));
+        CUDA_TRY(cudaMemcpyAsync(o + e0, dout + e0, ne * 4, cudaMemcpyDeviceToHost, d2h));
+        if (m_out) CUDA_TRY(cudaMemcpyAsync(m_out + r0, dm + r0, nr * 4, cudaMemcpyDeviceToHost, d2h));
+        if (l_out) CUDA_TRY(cudaMemcpyAsync(l_out + r0, dl + r0, nr * 4, cudaMemcpyDeviceToHost, d2h));
+    }
+    std::vector<efta_counters> hc(nchunk);
+    for (int c = 0; c < nchunk; ++c)
+        CUDA_TRY(cudaMemcpyAsync(&hc[c], reinterpret_cast<char*>(dcnt) + c * cnt_stride, sizeof(efta_counters),
+                                 cudaMemcpyDeviceToHost, d2h));
+    CUDA_TRY(cudaStreamSynchronize(d2h));
+    // merge the chunks' counters and events (event heads back to the flat index)
+    efta_counters tot{};
+    int n_ev = 0;
+    for (int c = 0; c < nchunk; ++c) {
+        const efta_counters& x = hc[c];
+        tot.n_fired += x.n_fired;
+        tot.detections += x.detections;
+        tot.corrections += x.corrections;
+        tot.recomputes += x.recomputes;
+        tot.range_replacements += x.range_replacements;
+        tot.failed |= x.failed;
+        for (int f = 0; f < 3; ++f) tot.family_max[f] = std::max(tot.family_max[f], x.family_max[f]);
+        if (events && ev_cap > 0 && x.n_events > 0) {
+            const int take_n = std::min(x.n_events, ev_cap - n_ev);
+            if (take_n > 0) {
+                const char* src = reinterpret_cast<const char*>(de) + c * ev_stride;
+                CUDA_TRY(cudaMemcpy(events + n_ev, src, sizeof(efta_event) * take_n, cudaMemcpyDeviceToHost));
+                for (int i = 0; i < take_n; ++i) events[n_ev + i].head += c * per;
+                n_ev += take_n;
+            }
+        }
+        tot.n_events += x.n_events;
+    }
+    if (counters) *counters = tot;
+    if (fired && fired_cap > 0 && tot.n_fired > 0)
+        CUDA_TRY(cudaMemcpy(fired, dfi, sizeof(efta_fired) * std::min(tot.n_fired, fired_cap), cudaMemcpyDeviceToHost));
     return 0;
 }
 
