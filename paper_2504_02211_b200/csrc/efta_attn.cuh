@@ -70,7 +70,7 @@ struct AttnParams {
 // phase timestamps (clock64) of CTAs (2,5) and (3,5): row warp 4 lane 0 and the MMA thread
 #define EFTA_TS(slot, j)                                                                       \
     do {                                                                                       \
-        if (p.prof && (blockIdx.x == 2 || blockIdx.x == 3) && blockIdx.y == 5 &&                 \
+        if (p.prof && (blockIdx.x == 2 || blockIdx.x == 3) && (blockIdx.y == 5 || gridDim.y == 1) && \
             (threadIdx.x & 31) == 0 && (j) >= 0 && (j) < 64)                                               \
             p.prof[(j) * 32 + (blockIdx.x & 1) * 16 + (slot)] = clock64();                       \
     } while (0)

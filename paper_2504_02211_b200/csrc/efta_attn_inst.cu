@@ -4,6 +4,8 @@
 #include "efta_attn_pair.cuh"
 #include "efta_launch.h"
 
+#include <algorithm>
+
 #ifndef EFTA_INST_D
 #error "EFTA_INST_D must be 64 or 128"
 #endif
@@ -56,8 +58,16 @@ cudaError_t launch_pair_t(const CUtensorMap& tka, const CUtensorMap& tkb,
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    dim3 grid(p.nblk, bh);
-    kern<<<grid, 384, PL::SMEM_BYTES, st>>>(tka, tkb, tkc, tvt, p);
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // persistent: one CTA pair per TPC (two SMs), each walking (head, query-tile pair) items
+    const long long items = static_cast<long long>(p.nblk / 2) * bh;
+    const int clusters = static_cast<int>(std::min<long long>(items, nsm / 2));
+    kern<<<dim3(2 * clusters), kPairThreads, PL::SMEM_BYTES, st>>>(tka, tkb, tkc, tvt, p);
     return cudaGetLastError();
 }
 

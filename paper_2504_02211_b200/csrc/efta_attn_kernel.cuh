@@ -808,7 +808,7 @@ template <int D, int MODE, bool DBG>
 __global__ void __launch_bounds__(attn_threads(MODE, DBG), 1)
 efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
-                     const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
+                     const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ AttnParams p) {
     using L = AttnLayout<D>;
     constexpr bool PROT = MODE != EFTA_MODE_NONE;
     constexpr int KS = L::KS, VS = L::VS, NSUB = L::NSUB;

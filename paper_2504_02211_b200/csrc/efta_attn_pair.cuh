@@ -30,6 +30,10 @@
 
 namespace efta_sm100 {
 
+// warps: 0 TMA producer, 1 score-MMA issuer, 2 P.V-MMA issuer, 3..10 row warps
+// (two row warpgroups: warps 3-6 = half 0, 7-10 = half 1; warp w reads TMEM lanes 32*(w%4))
+constexpr int kPairThreads = 352;
+
 template <int D, bool PROT>
 struct PairLayout {
     static constexpr int NSUB = D / 64;
@@ -45,7 +49,7 @@ struct PairLayout {
     static constexpr uint32_t OFF_K = 0;
     static constexpr uint32_t OFF_V = OFF_K + KS * K_STAGE;
     static constexpr uint32_t OFF_BAR = OFF_V + VS * V_STAGE;
-    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2 + 2;
+    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 3 + 2 + 1;
     static constexpr uint32_t OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
     static constexpr uint32_t RED_BYTES = 128 * 24 + 256;
@@ -103,38 +107,25 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* tma
         : "memory");
 }
 
-// Row warps: copy this CTA's 128 query rows into the TMEM A-operand columns (fp16
-// pairs, column x = dims 2x, 2x+1); half h stages dims [D/2*h, D/2*(h+1)).
-template <int D>
-__device__ __forceinline__ void stage_q_tmem(const AttnParams& p, uint32_t tmem, uint32_t col_q, int warp,
-                                             int lane, int seq_row0, int qt) {
-    const int half = (warp - 4) >> 2, wq = warp & 3, row = wq * 32 + lane;
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-    const uint4* src = reinterpret_cast<const uint4*>(p.q + (static_cast<size_t>(seq_row0) + qt * kBlock + row) * D +
-                                                      half * (D / 2));
-    constexpr int W = D / 4;  // 32-bit columns per half
-    uint32_t w[W];
-#pragma unroll
-    for (int i = 0; i < W / 4; ++i) {
-        const uint4 u = __ldg(src + i);
-        w[4 * i] = u.x;
-        w[4 * i + 1] = u.y;
-        w[4 * i + 2] = u.z;
-        w[4 * i + 3] = u.w;
-    }
-    if constexpr (W == 32) tmem_st32(lane_base + col_q + half * W, w);
-    else tmem_st16(lane_base + col_q + half * W, w);
-    tmem_wait_st();
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+                 : "memory");
 }
 
+// Persistent pair kernel: grid = 2 x (clusters), each cluster walks the work items
+// it = cluster, cluster + C, ... ; item = (head, pair of 128-row query tiles), the CTA of
+// rank r owns query tile 2*(it % (n/2)) + r. Ring stages and barrier phases run on a
+// global key-block counter g = t*n + j (t = the cluster's item ordinal), so the producers
+// stream the next item's K/V while the row warps finish the current one, and the next
+// item's first score MMAs overlap the current item's epilogue.
 // tm_ka: K rows [0, HN_S) of each block (leader; [64r, 64r+64) unprotected), tm_kb: K rows
 // 72..127 (peer, protected), tm_kc: KC rows in 8-row boxes (protected), tm_vt: [V^T ; VC^T]
 // rows of each block, box rows HN_V.
 template <int D, int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_ka, const __grid_constant__ CUtensorMap tm_kb,
                       const __grid_constant__ CUtensorMap tm_kc, const __grid_constant__ CUtensorMap tm_vt,
-                      const AttnParams p) {
+                      const __grid_constant__ AttnParams p) {
     constexpr bool PROT = MODE != EFTA_MODE_NONE;
     using L = PairLayout<D, PROT>;
     constexpr int KS = L::KS, VS = L::VS, NSUB = L::NSUB;
@@ -148,15 +139,23 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_ka, const __grid_co
     uint64_t* v_full = k_empty + KS;
     uint64_t* v_empty = v_full + VS;
     uint64_t* s_full = v_empty + VS;
+    // p_ready[g&1]: row warps of different slices / CTAs are not in lockstep, so a fast
+    // warp may arrive for block g+1 before block g's phase completed; alternating barriers
+    // keep the counts apart (a warp cannot reach g+2 before PV(g), hence p_ready[g&1], ran)
     uint64_t* p_ready = s_full + 2;
-    uint64_t* o_done = p_ready + 1;
-    uint64_t* pv_done = o_done + 1;  // [2]: PV(j) done, per S buffer j&1
+    uint64_t* o_done = p_ready + 2;
+    uint64_t* pv_done = o_done + 1;  // [2]: PV(g) done, per S buffer g&1
+    uint64_t* o_free = pv_done + 2;  // O read out of TMEM by both CTAs' row warps
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
     const int warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_rank();
-    const int qt = blockIdx.x, head = blockIdx.y, n = p.nblk;
-    const int seq_row0 = head * p.seq_len;
+    const int n = p.nblk;
+    const int pairs_per_head = n / 2;
+    const int total = pairs_per_head * p.n_heads_flat;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    auto item_head = [&](int it) { return it / pairs_per_head; };
+    auto item_qt = [&](int it) { return 2 * (it % pairs_per_head) + static_cast<int>(rank); };
 
     if (warp == 0 && lane == 0) {
         mbar_init(q_ready, 16);  // 8 row warps x 2 CTAs
@@ -164,10 +163,12 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_ka, const __grid_co
         for (int s = 0; s < VS; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
         mbar_init(&s_full[0], 1);
         mbar_init(&s_full[1], 1);
-        mbar_init(p_ready, 16);  // 8 row warps x 2 CTAs
+        mbar_init(&p_ready[0], 16);  // 8 row warps x 2 CTAs
+        mbar_init(&p_ready[1], 16);
         mbar_init(o_done, 1);
         mbar_init(&pv_done[0], 1);
         mbar_init(&pv_done[1], 1);
+        mbar_init(o_free, 16);
         fence_barrier_init();
         tma_prefetch_desc(&tm_ka);
         tma_prefetch_desc(&tm_vt);
@@ -183,50 +184,56 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_ka, const __grid_co
     const uint32_t v_smem = smem_u32(smem + L::OFF_V);
 
     if (warp == 0) {
-        // -------------------------------------------------------- K (+KC1) half producer
+        // -------------------------------------------------------- K (+KC1) / V^T (+VC^T) producer
+        // one thread streams both rings in block order (K(g) is consumed before V(g))
         if (lane == 0) {
-            for (int j = 0; j < n; ++j) {
-                const int s = j % KS;
-                mbar_wait(&k_empty[s], ((j / KS) & 1) ^ 1);
-                uint8_t* dst = smem + L::OFF_K + s * L::K_STAGE;
-#ifdef EFTA_NO_TMA  // experiment build: MMAs on stale tiles, no K/V traffic
-                if (rank == 0) mbar_arrive(&k_full[s]);
-                continue;
-#endif
-                if (rank == 0) mbar_arrive_expect_tx(&k_full[s], 2 * L::K_STAGE);
-                const int krow = seq_row0 + j * kBlock;
-#pragma unroll
-                for (int sub = 0; sub < NSUB; ++sub) {
-                    uint8_t* c = dst + sub * L::K_CHUNK;
-                    if (!PROT) {
-                        tma_load_2d_pair(c, &tm_ka, &k_full[s], sub * 64, krow + 64 * rank, kEvictLast);
-                    } else if (rank == 0) {
-                        tma_load_2d_pair(c, &tm_ka, &k_full[s], sub * 64, krow, kEvictLast);
-                    } else {
-                        const int crow = (head * n + j) * 32;
-                        tma_load_2d_pair(c, &tm_kb, &k_full[s], sub * 64, krow + 72, kEvictLast);
-                        tma_load_2d_pair(c + 56 * 128, &tm_kc, &k_full[s], sub * 64, crow, kEvictLast);      // c1_hi
-                        tma_load_2d_pair(c + 64 * 128, &tm_kc, &k_full[s], sub * 64, crow + 16, kEvictLast); // c1_lo
+            for (int t = 0, it = cid; it < total; ++t, it += ncl) {
+                const int head = item_head(it);
+                const int seq_row0 = head * p.seq_len;
+                for (int j = 0; j < n; ++j) {
+                    const int g = t * n + j;
+                    const int s = g % KS;
+                    mbar_wait(&k_empty[s], ((g / KS) & 1) ^ 1);
+                    if (j == (n > 8 ? n - 8 : 0) && it + ncl < total) {  // next item's Q rows -> L2
+                        const int nit = it + ncl;
+                        prefetch_l2_bulk(p.q + (static_cast<size_t>(item_head(nit)) * p.seq_len +
+                                                static_cast<size_t>(item_qt(nit)) * kBlock) * D,
+                                         kBlock * D * 2);
                     }
-                }
-            }
-        }
-    } else if (warp == 3) {
-        // -------------------------------------------------------- V^T (+VC^T) half producer
-        if (lane == 0) {
-            for (int j = 0; j < n; ++j) {
-                const int s = j % VS;
-                mbar_wait(&v_empty[s], ((j / VS) & 1) ^ 1);
-                uint8_t* dst = smem + L::OFF_V + s * L::V_STAGE;
-#ifdef EFTA_NO_TMA
-                if (rank == 0) mbar_arrive(&v_full[s]);
-                continue;
-#endif
-                if (rank == 0) mbar_arrive_expect_tx(&v_full[s], 2 * L::V_STAGE);
-                const int vrow = (head * n + j) * L::VROWS + L::HN_V * rank;
+                    uint8_t* dst = smem + L::OFF_K + s * L::K_STAGE;
+#ifdef EFTA_NO_TMA  // experiment build: MMAs on stale tiles, no K/V traffic
+                    if (rank == 0) mbar_arrive(&k_full[s]);
+#else
+                    if (rank == 0) mbar_arrive_expect_tx(&k_full[s], 2 * L::K_STAGE);
+                    const int krow = seq_row0 + j * kBlock;
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
-                    tma_load_2d_pair(dst + c * L::V_CHUNK, &tm_vt, &v_full[s], c * 64, vrow, kEvictLast);
+                    for (int sub = 0; sub < NSUB; ++sub) {
+                        uint8_t* c = dst + sub * L::K_CHUNK;
+                        if (!PROT) {
+                            tma_load_2d_pair(c, &tm_ka, &k_full[s], sub * 64, krow + 64 * rank, kEvictLast);
+                        } else if (rank == 0) {
+                            tma_load_2d_pair(c, &tm_ka, &k_full[s], sub * 64, krow, kEvictLast);
+                        } else {
+                            const int crow = (head * n + j) * 32;
+                            tma_load_2d_pair(c, &tm_kb, &k_full[s], sub * 64, krow + 72, kEvictLast);
+                            tma_load_2d_pair(c + 56 * 128, &tm_kc, &k_full[s], sub * 64, crow, kEvictLast);      // c1_hi
+                            tma_load_2d_pair(c + 64 * 128, &tm_kc, &k_full[s], sub * 64, crow + 16, kEvictLast); // c1_lo
+                        }
+                    }
+#endif
+                    const int sv = g % VS;
+                    mbar_wait(&v_empty[sv], ((g / VS) & 1) ^ 1);
+                    uint8_t* vdst = smem + L::OFF_V + sv * L::V_STAGE;
+#ifdef EFTA_NO_TMA
+                    if (rank == 0) mbar_arrive(&v_full[sv]);
+#else
+                    if (rank == 0) mbar_arrive_expect_tx(&v_full[sv], 2 * L::V_STAGE);
+                    const int vrow = (head * n + j) * L::VROWS + L::HN_V * rank;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+                        tma_load_2d_pair(vdst + c * L::V_CHUNK, &tm_vt, &v_full[sv], c * 64, vrow, kEvictLast);
+#endif
+                }
             }
         }
     } else if (warp == 1) {
@@ -238,27 +245,32 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_ka, const __grid_co
         if (lane == 0 && rank == 0) {
             constexpr uint32_t ID_S = idesc_f16_f32(256, L::NS, 0, 0);
             const uint32_t a_q = tmem + L::COL_Q;
-            mbar_wait(q_ready, 0);
-            tc_fence_after();
-            for (int j = 0; j < n; ++j) {
-                const int s = j % KS;
-                if (j >= 2) {  // S[j&1] holds P(j-2) until PV(j-2) has read it
-                    mbar_wait(&pv_done[j & 1], ((j >> 1) + 1) & 1);
+            for (int t = 0, it = cid; it < total; ++t, it += ncl) {
+                for (int j = 0; j < n; ++j) {
+                    const int g = t * n + j;
+                    const int s = g % KS;
+                    if (j == 0) {  // this item's Q staged in TMEM by both CTAs
+                        mbar_wait(q_ready, t & 1);
+                        tc_fence_after();
+                    }
+                    if (g >= 2) {  // S[g&1] holds P(g-2) until PV(g-2) has read it
+                        mbar_wait(&pv_done[g & 1], ((g >> 1) + 1) & 1);
+                        tc_fence_after();
+                    }
+                    mbar_wait(&k_full[s], (g / KS) & 1);
+                    EFTA_TS(9, j);
                     tc_fence_after();
-                }
-                mbar_wait(&k_full[s], (j / KS) & 1);
-                EFTA_TS(9, j);
-                tc_fence_after();
-                const uint32_t kb = k_smem + s * L::K_STAGE;
-                const uint32_t d_s = tmem + L::COL_S0 + (j & 1) * L::S_STRIDE;
+                    const uint32_t kb = k_smem + s * L::K_STAGE;
+                    const uint32_t d_s = tmem + L::COL_S0 + (g & 1) * L::S_STRIDE;
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t offk = (kk >> 2) * L::K_CHUNK + (kk & 3) * 32;
-                    mma2_ts(d_s, a_q + kk * 8, smem_desc_sw128(kb + offk, 16, 1024), ID_S, kk > 0);
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t offk = (kk >> 2) * L::K_CHUNK + (kk & 3) * 32;
+                        mma2_ts(d_s, a_q + kk * 8, smem_desc_sw128(kb + offk, 16, 1024), ID_S, kk > 0);
+                    }
+                    commit2_both(&k_empty[s]);
+                    commit2_both(&s_full[g & 1]);
+                    EFTA_TS(11, j);
                 }
-                commit2_both(&k_empty[s]);
-                commit2_both(&s_full[j & 1]);
-                EFTA_TS(11, j);
             }
         }
         __syncwarp();
@@ -266,41 +278,53 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_ka, const __grid_co
         // -------------------------------------------------------- P.V MMA issuer (pair leader)
         if (lane == 0 && rank == 0) {
             constexpr uint32_t ID_PV = idesc_f16_f32(256, L::VROWS, 0, 0);
-            for (int j = 0; j < n; ++j) {
-                EFTA_TS(10, j);
-                mbar_wait(p_ready, j & 1);
-                EFTA_TS(12, j);
-                tc_fence_after();
-                const int s = j % VS;
-                mbar_wait(&v_full[s], (j / VS) & 1);
-                EFTA_TS(14, j);
-                tc_fence_after();
-                const uint32_t vb = v_smem + s * L::V_STAGE;
-                const uint32_t a_p = tmem + L::COL_S0 + (j & 1) * L::S_STRIDE;
+            for (int t = 0, it = cid; it < total; ++t, it += ncl) {
+                for (int j = 0; j < n; ++j) {
+                    const int g = t * n + j;
+                    EFTA_TS(10, j);
+                    mbar_wait(&p_ready[g & 1], (g >> 1) & 1);
+                    EFTA_TS(12, j);
+                    tc_fence_after();
+                    const int s = g % VS;
+                    mbar_wait(&v_full[s], (g / VS) & 1);
+                    if (j == 0 && t > 0) mbar_wait(o_free, (t - 1) & 1);  // previous item's O read out
+                    EFTA_TS(14, j);
+                    tc_fence_after();
+                    const uint32_t vb = v_smem + s * L::V_STAGE;
+                    const uint32_t a_p = tmem + L::COL_S0 + (g & 1) * L::S_STRIDE;
 #pragma unroll
-                for (int kk = 0; kk < kBlock / 16; ++kk) {
-                    const uint32_t offv = (kk >> 2) * L::V_CHUNK + (kk & 3) * 32;
-                    mma2_ts(tmem + L::COL_O, a_p + kk * 8, smem_desc_sw128(vb + offv, 16, 1024), ID_PV,
-                            (j > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < kBlock / 16; ++kk) {
+                        const uint32_t offv = (kk >> 2) * L::V_CHUNK + (kk & 3) * 32;
+                        mma2_ts(tmem + L::COL_O, a_p + kk * 8, smem_desc_sw128(vb + offv, 16, 1024), ID_PV,
+                                (j > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    commit2_both(&v_empty[s]);
+                    commit2_both(&pv_done[g & 1]);
+                    commit2_both(o_done);
+                    EFTA_TS(13, j);
                 }
-                commit2_both(&v_empty[s]);
-                commit2_both(&pv_done[j & 1]);
-                commit2_both(o_done);
-                EFTA_TS(13, j);
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
-        stage_q_tmem<D>(p, tmem, L::COL_Q, warp, lane, seq_row0, qt);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(q_ready, 0);
+    } else if (warp >= kRowWarp0) {
         RowScratch rs;
         rs.slots = reinterpret_cast<RowSlot*>(smem + L::OFF_RED);
         rs.ints = reinterpret_cast<int*>(smem + L::OFF_RED + 128 * sizeof(RowSlot));
         rs.dbl = reinterpret_cast<double*>(smem + L::OFF_RED + 128 * sizeof(RowSlot) + 16 * sizeof(int));
-        row_split<D, MODE, true, L>(p, s_full, p_ready, o_done, tmem, warp, lane, head, qt, n, seq_row0, rs,
-                                    reinterpret_cast<float*>(smem + L::OFF_XCH));
+        if (cid < total) {
+            stage_q_rows<D>(p, tmem + L::COL_Q, warp, lane, item_head(cid) * p.seq_len + item_qt(cid) * kBlock);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(q_ready, 0);
+        }
+        for (int t = 0, it = cid; it < total; ++t, it += ncl) {
+            const int head = item_head(it), qt = item_qt(it);
+            const int nit = it + ncl;
+            const int next_q_row = nit < total ? item_head(nit) * p.seq_len + item_qt(nit) * kBlock : -1;
+            row_split<D, MODE, true, L>(p, s_full, p_ready, o_done, o_free, tmem, warp, lane, head, qt, n,
+                                        head * p.seq_len, t * n, rs, reinterpret_cast<float*>(smem + L::OFF_XCH),
+                                        next_q_row, q_ready);
+        }
     }
 
     tc_fence_before();

@@ -38,6 +38,8 @@ __device__ __forceinline__ uint32_t sm_id() {
     return r;
 }
 
+constexpr int kRowWarp0 = 3;  // first row warp of the pair kernel (warps 3..10)
+
 // named barrier ids of the split schedule (0 = __syncthreads, 1..7 = half-0 helpers)
 constexpr uint32_t kBarPair0 = 8;   // 8..11: per row slice (warps w, w+4), 64 threads
 constexpr uint32_t kBarTile = 12;   // all 256 row threads
@@ -50,6 +52,29 @@ struct SplitXch {
     static constexpr uint32_t BYTES = FLOATS * 4;
 };
 
+// Row warps: copy 128 query rows (from global row q_row0) into the TMEM A-operand columns
+// (fp16 pairs, column x = dims 2x, 2x+1); half h stages dims [D/2*h, D/2*(h+1)).
+template <int D>
+__device__ __forceinline__ void stage_q_rows(const AttnParams& p, uint32_t col_q_addr, int warp, int lane,
+                                             int q_row0) {
+    const int half = (warp - kRowWarp0) >> 2, wq = warp & 3, row = wq * 32 + lane;
+    const uint32_t lane_base = col_q_addr + (static_cast<uint32_t>(wq * 32) << 16);
+    const uint4* src = reinterpret_cast<const uint4*>(p.q + (static_cast<size_t>(q_row0) + row) * D + half * (D / 2));
+    constexpr int W = D / 4;  // 32-bit columns per half
+    uint32_t w[W];
+#pragma unroll
+    for (int i = 0; i < W / 4; ++i) {
+        const uint4 u = __ldg(src + i);
+        w[4 * i] = u.x;
+        w[4 * i + 1] = u.y;
+        w[4 * i + 2] = u.z;
+        w[4 * i + 3] = u.w;
+    }
+    if constexpr (W == 32) tmem_st32(lane_base + half * W, w);
+    else tmem_st16(lane_base + half * W, w);
+    tmem_wait_st();
+}
+
 template <bool PAIR>
 __device__ __forceinline__ void split_signal_p_ready(uint64_t* bar, int lane) {
     __syncwarp();
@@ -61,16 +86,89 @@ __device__ __forceinline__ void split_signal_p_ready(uint64_t* bar, int lane) {
 
 // TL: TMEM plan (COL_S0, S_STRIDE, COL_O); the score checksum columns are the pair
 // layout (cols 128..135 c1_hi, 136..143 c1_lo).
+// Rare exp-stage ladder of one (i, j) tile for the split schedule: both halves have
+// dumped their 64 P values of the row into the per-SM scratch row; half 0 runs the
+// reference ladder (exp_stage_slow) over the full rows and publishes the repaired max,
+// block max and a replaced flag through xpub (P rows rewritten in the scratch).
+template <int D>
+__device__ __noinline__ float2 split_exp_rare(const AttnParams& p, uint32_t s_addr, uint32_t cs_addr, int head,
+                                              int qt, int j, int row, int half, bool exp_affected, int exp_viol,
+                                              float m_run, float m_new, float bm, float* xpub,
+                                              const RowScratch& rs) {
+    float* scr = p.scratch + static_cast<size_t>(sm_id()) * (128 * 128) + row * 128;
+    if (half == 1) {
+        xpub[row * 4 + 0] = exp_affected ? 1.0f : 0.0f;
+        xpub[row * 4 + 1] = static_cast<float>(exp_viol);
+    }
+    named_bar_sync(kBarRare, 256);
+    if (half == 0) {
+        const bool aff = exp_affected || xpub[row * 4 + 0] != 0.0f;
+        const int viol = exp_viol + static_cast<int>(xpub[row * 4 + 1]);
+        float p_loc[kBlock];
+        for (int c = 0; c < kBlock; ++c) p_loc[c] = scr[c];
+        int replaced = 0;
+        ThreadTap no_tap{};
+        exp_stage_slow<false, D>(p, s_addr, cs_addr, head, qt, j, row, aff, isfinite(m_new) ? 0.0f : CUDART_INF_F,
+                                 viol, m_run, m_new, bm, p_loc, replaced, no_tap, -1, 0.0f, rs);
+        if (replaced) {
+            for (int c = 0; c < kBlock; ++c) scr[c] = p_loc[c];
+        }
+        xpub[row * 4 + 0] = m_new;
+        xpub[row * 4 + 1] = bm;
+        xpub[row * 4 + 2] = replaced ? 1.0f : 0.0f;
+    }
+    named_bar_sync(kBarRare, 256);
+    return make_float2(xpub[row * 4 + 0], xpub[row * 4 + 1]);
+}
+
+// Rare final output correction (verify_locate_correct on O, abft.cpp:65-187) for the split
+// schedule: both halves have dumped their normalised O columns into the per-SM scratch
+// row; half 0 verifies / corrects the full rows in place and reports the tile event.
+template <int D>
+__device__ __noinline__ float split_out_rare(const AttnParams& p, int head, int qt, int n, int row, int half,
+                                             bool viol, bool cs_bad, double res, const float* c1, const float* c2,
+                                             double eps_mult, const RowScratch& rs) {
+    float* scr = p.scratch + static_cast<size_t>(sm_id()) * (128 * 128) + row * 128;
+    named_bar_sync(kBarRare, 256);
+    float fam_out = static_cast<float>(res);
+    if (half == 0) {
+        const bool tcs = named_bar_or(4, 128, cs_bad);
+        RowVerify rv{};
+        rv.best_col = -1;
+        rv.restored_col = -1;
+        rv.residual = res;
+        float full[D], cc1[kStride], cc2[kStride];
+        for (int c = 0; c < D; ++c) full[c] = scr[c];
+        for (int x = 0; x < kStride; ++x) { cc1[x] = c1[x]; cc2[x] = c2[x]; }
+        if (!tcs && viol) verify_row<D>(full, cc1, cc2, p.eps2 * eps_mult, rv);
+        for (int c = 0; c < D; ++c) scr[c] = full[c];
+        fam_out = static_cast<float>(rv.residual);
+        TileReport tr = reduce_tile_report(rv, tcs, row, rs.slots, rs.ints, rs.dbl);
+        if (row == 0)
+            push_event(p, EFTA_OUTPUT_CHECKSUM, head, qt, n, tr.status, tr.row, tr.col, tr.violations,
+                       tr.corrections, tr.checksum_repair, tr.residual, tr.delta);
+    }
+    named_bar_sync(kBarRare, 256);
+    return fam_out;
+}
+
+// One (head, query tile) work item of a persistent CTA. g0: global key-block counter of
+// this item's j = 0 (ring / barrier phases run on across items); next_q_row (>= 0): first
+// global query row of the next item, staged into TMEM once every score MMA of this item has
+// completed (so the next item's first score MMAs overlap this epilogue); o_free: arrived on once O
+// has been read out of TMEM (the next item's first P.V may overwrite it). p_ready is
+// the pair [2] indexed by block parity.
 template <int D, int MODE, bool PAIR, class TL>
 __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full, uint64_t* p_ready,
-                                          uint64_t* o_done, uint32_t tmem, int warp, int lane,
-                                          int head, int qt, int n, int seq_row0, const RowScratch& rs,
-                                          float* xch) {
+                                          uint64_t* o_done, uint64_t* o_free, uint32_t tmem, int warp,
+                                          int lane, int head, int qt, int n, int seq_row0, int g0,
+                                          const RowScratch& rs, float* xch, int next_q_row,
+                                          uint64_t* q_ready) {
     using L = TL;
     constexpr bool PROT = MODE != EFTA_MODE_NONE;
     constexpr int DH = D / 2;          // O columns per half
     constexpr int GH = DH / kStride;   // output groups per half
-    const int half = (warp - 4) >> 2;  // warp-uniform
+    const int half = (warp - kRowWarp0) >> 2;  // warp-uniform
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
     const uint32_t bar_pair = kBarPair0 + wq;
@@ -80,31 +178,27 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
     float* xprod = xch + SplitXch::XPROD;
     float* xpub = xch + SplitXch::XPUB;
     float* xl = xch + SplitXch::XL;
-    float* scr = p.scratch + static_cast<size_t>(sm_id()) * (128 * 128) + row * 128;  // rare paths
+    // per-SM scratch row of the rare paths (computed there: keeps the hot loop's registers free)
+#define EFTA_SCR (p.scratch + static_cast<size_t>(sm_id()) * (128 * 128) + row * 128)
     const float scale = p.scale, scale_log2 = p.scale_log2;
     // m_run: the max P is referenced to (lazy); m_true: the running row max (reference m)
     float m_run = -CUDART_INF_F, m_true = -CUDART_INF_F, l_half = 0.0f, lb = 0.0f;
-    ThreadTap no_tap{};
 
     for (int j = 0; j < n; ++j) {
-        const int b = j & 1;
+        const int g = g0 + j;
+        const int b = g & 1;
         const uint32_t s_addr = lane_base + L::COL_S0 + b * L::S_STRIDE;
         const uint32_t cs_addr = s_addr + 128;
         if (warp == 4) EFTA_TS(0, j);
-        mbar_wait(&s_full[b], (j >> 1) & 1);
+        mbar_wait(&s_full[b], (g >> 1) & 1);
         if (warp == 4) EFTA_TS(1, j);
         tc_fence_after();
 #ifdef EFTA_MMA_ONLY  // experiment build: tensor-pipe / operand-feed bound of the schedule
-        if (true) { split_signal_p_ready<PAIR>(p_ready, lane); continue; }
+        if (true) { split_signal_p_ready<PAIR>(&p_ready[g & 1], lane); continue; }
 #endif
         float pv[64];
-        uint32_t c1h[4], c1l[4];
         tmem_ld32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(&pv[0]));
         tmem_ld32(s_addr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&pv[32]));
-        if (PROT) {  // c1 (hi, lo) of this half's checked groups x = 4*half .. 4*half+3
-            tmem_ld4(cs_addr + 4 * half, c1h);
-            tmem_ld4(cs_addr + 8 + 4 * half, c1l);
-        }
         tmem_wait_ld();
         // ---- row max: partial over this half, exchanged within the row slice
         float mx0 = pv[0], mx1 = pv[1], mx2 = pv[2], mx3 = pv[3];
@@ -124,15 +218,6 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
         m_true = (m_true < bm) ? bm : m_true;
         float m_new = (j == 0 || m_true - m_run > kLazyTau) ? m_true : m_run;
         const float mL = m_new * kLog2e;
-        float pc1v[4];
-        if (PROT) {  // Pc1 = exp(scale*c1 - 16 m): these MUFUs overlap the loop below
-            const float g16m = 16.0f * m_new;
-#pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                const float c1 = __fadd_rn(__uint_as_float(c1h[x]), __uint_as_float(c1l[x]));
-                pc1v[x] = ex2_approx(__fsub_rn(__fmul_rn(c1, scale), g16m) * kLog2e);
-            }
-        }
         // ---- exponentials (MUFU + FMA-pipe polynomial), fused row sum and group products
         const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
         float2 ps0 = make_float2(0.0f, 0.0f), ps1 = make_float2(0.0f, 0.0f);
@@ -161,12 +246,28 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
         bool exp_affected = false, factor_bad = false;
         int exp_viol = 0;
         if (PROT) {
+            // c1 (hi, lo) of this half's checked groups x = 4*half .. 4*half+3 (loaded after the
+            // exponentials: keeps them out of the loop's register footprint)
+            uint32_t c1h[4], c1l[4];
+            tmem_ld4(cs_addr + 4 * half, c1h);
+            tmem_ld4(cs_addr + 8 + 4 * half, c1l);
             // hand the partner the partial products of its groups, complete our own
             float* xp = xprod + b * 1024;
             const float4 send = half == 0 ? make_float4(prod[2].x, prod[2].y, prod[3].x, prod[3].y)
                                           : make_float4(prod[0].x, prod[0].y, prod[1].x, prod[1].y);
             *reinterpret_cast<float4*>(&xp[(half * 128 + row) * 4]) = send;
+            tmem_wait_ld();
+            float pc1v[4];  // Pc1 = exp(scale*c1 - 16 m)
+            {
+                const float g16m = 16.0f * m_new;
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    const float c1 = __fadd_rn(__uint_as_float(c1h[x]), __uint_as_float(c1l[x]));
+                    pc1v[x] = ex2_approx(__fsub_rn(__fmul_rn(c1, scale), g16m) * kLog2e);
+                }
+            }
             named_bar_sync(bar_pair, 64);
+            if (warp == 4) EFTA_TS(5, j);
             const float4 rv = *reinterpret_cast<const float4*>(&xp[((1 - half) * 128 + row) * 4]);
             const float2 own0 = half == 0 ? prod[0] : prod[2], own1 = half == 0 ? prod[1] : prod[3];
             const float pr[4] = {own0.x * rv.x, own0.y * rv.y, own1.x * rv.z, own1.y * rv.w};
@@ -177,38 +278,26 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
             if (j > 0) factor_bad = !(f > 0.0f && f <= 1.0f);  // NaN fails both
         }
         float psum = (ps0.x + ps0.y) + (ps1.x + ps1.y);
-        if (PROT && named_bar_or(kBarTile, 256, exp_affected || factor_bad)) {
-            // ---- rare: exp-stage ladder + factor guard over the full rows on half 0
-            if (half == 1) {
+        const bool tile_trig = PROT && named_bar_or(kBarTile, 256, exp_affected || factor_bad);
+        if (warp == 4) EFTA_TS(7, j);
+        if (tile_trig) {
+            // ---- rare: exp-stage ladder + factor guard over the full rows (out of line: the
+            // row halves go through the per-SM scratch so P stays in registers here)
 #pragma unroll
-                for (int c = 0; c < 64; ++c) scr[64 + c] = pv[c];
-                xpub[row * 4 + 0] = exp_affected ? 1.0f : 0.0f;
-                xpub[row * 4 + 1] = static_cast<float>(exp_viol);
-            }
-            named_bar_sync(kBarRare, 256);
-            if (half == 0) {
-                const bool aff = exp_affected || xpub[row * 4 + 0] != 0.0f;
-                const int viol = exp_viol + static_cast<int>(xpub[row * 4 + 1]);
-                float p_loc[kBlock];
-                for (int c = 0; c < 64; ++c) { p_loc[c] = pv[c]; p_loc[64 + c] = scr[64 + c]; }
-                int replaced = 0;
-                exp_stage_slow<false, D>(p, s_addr, cs_addr, head, qt, j, row, aff, isfinite(m_new) ? 0.0f : CUDART_INF_F,
-                                      viol, m_run, m_new, bm, p_loc, replaced, no_tap, -1, 0.0f, rs);
-                if (replaced) {
-                    for (int c = 0; c < 64; ++c) { pv[c] = p_loc[c]; scr[64 + c] = p_loc[64 + c]; }
-                }
-                xpub[row * 4 + 0] = m_new;
-                xpub[row * 4 + 1] = bm;
-                xpub[row * 4 + 2] = replaced ? 1.0f : 0.0f;
-            }
-            named_bar_sync(kBarRare, 256);
-            m_new = xpub[row * 4 + 0];
-            bm = xpub[row * 4 + 1];
+            for (int c = 0; c < 64; ++c) EFTA_SCR[half * 64 + c] = pv[c];
+#ifdef EFTA_NO_RARE_CALL
+            const float2 mb = make_float2(m_new, bm); __trap();
+#else
+            const float2 mb = split_exp_rare<D>(p, s_addr, cs_addr, head, qt, j, row, half, exp_affected, exp_viol,
+                                                m_run, m_new, bm, xpub, rs);
+#endif
+            m_new = mb.x;
+            bm = mb.y;
             if (xpub[row * 4 + 2] != 0.0f) {
-                if (half == 1) {
-                    for (int c = 0; c < 64; ++c) pv[c] = scr[64 + c];
-                }
+#pragma unroll
+                for (int c = 0; c < 64; ++c) pv[c] = EFTA_SCR[half * 64 + c];
                 float2 q0 = make_float2(pv[0], pv[1]), q1 = make_float2(pv[2], pv[3]);
+#pragma unroll
                 for (int c = 4; c < 64; c += 4) {
                     q0 = fadd2(q0, make_float2(pv[c], pv[c + 1]));
                     q1 = fadd2(q1, make_float2(pv[c + 2], pv[c + 3]));
@@ -234,7 +323,7 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
         // only when some row of the warp moved its reference max (lazy rescale)
         if (j > 0 && !__all_sync(0xffffffffu, f == 1.0f)) {
             if (warp == 4) EFTA_TS(4, j);
-            mbar_wait(o_done, (j - 1) & 1);
+            mbar_wait(o_done, (g - 1) & 1);
             tc_fence_after();
             constexpr int NO = DH / 32;
             constexpr int NCH = NO + (PROT ? 1 : 0);
@@ -261,13 +350,22 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
         }
         tmem_wait_st();
         tc_fence_before();
-        split_signal_p_ready<PAIR>(p_ready, lane);
+        split_signal_p_ready<PAIR>(&p_ready[g & 1], lane);
         if (warp == 4) EFTA_TS(6, j);
         m_run = m_new;
     }
 
+    if (next_q_row >= 0) {  // stage the next item's Q: every score MMA of this item has completed
+        stage_q_rows<D>(p, tmem + TL::COL_Q, warp, lane, next_q_row);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+            if constexpr (PAIR) mbar_arrive_cluster(q_ready, 0);
+            else mbar_arrive(q_ready);
+        }
+    }
     // ------------------------------------------------------------------ epilogue
-    mbar_wait(o_done, (n - 1) & 1);
+    mbar_wait(o_done, (g0 + n - 1) & 1);
     tc_fence_after();
     float o[DH];
     float c1[kStride], c2[kStride];
@@ -278,6 +376,12 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
         uint32_t oc[32];
         if (PROT && half == 0) tmem_ld32(lane_base + L::COL_O + D, oc);
         tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {  // O is in registers: the next item's first P.V may overwrite it
+            if constexpr (PAIR) mbar_arrive_cluster(o_free, 0);
+            else mbar_arrive(o_free);
+        }
 #pragma unroll
         for (int x = 0; x < kStride; ++x) {
             c1[x] = (PROT && half == 0) ? __fadd_rn(__uint_as_float(oc[x]), __uint_as_float(oc[16 + x])) : 0.0f;
@@ -387,33 +491,13 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
             fam_out = static_cast<float>(res);
         }
         if (named_bar_or(kBarTile, 256, viol || cs_bad)) {
-            // rare: locate / correct over the full rows on half 0
-            if (half == 1) {
+            // rare: locate / correct over the full rows (out of line, rows via the scratch)
 #pragma unroll
-                for (int c = 0; c < DH; ++c) scr[DH + c] = o[c];
-            }
-            named_bar_sync(kBarRare, 256);
-            if (half == 0) {
-                const bool tcs = named_bar_or(4, 128, cs_bad);
-                RowVerify rv{};
-                rv.best_col = -1;
-                rv.restored_col = -1;
-                rv.residual = res;
-                float full[D];
-                for (int c = 0; c < DH; ++c) { full[c] = o[c]; full[DH + c] = scr[DH + c]; }
-                if (!tcs && viol) verify_row<D>(full, c1, c2, p.eps2 * eps_mult, rv);
-                for (int c = 0; c < DH; ++c) { o[c] = full[c]; scr[DH + c] = full[DH + c]; }
-                fam_out = static_cast<float>(rv.residual);
-                TileReport tr = reduce_tile_report(rv, tcs, row, rs.slots, rs.ints, rs.dbl);
-                if (row == 0)
-                    push_event(p, EFTA_OUTPUT_CHECKSUM, head, qt, n, tr.status, tr.row, tr.col,
-                               tr.violations, tr.corrections, tr.checksum_repair, tr.residual, tr.delta);
-            }
-            named_bar_sync(kBarRare, 256);
-            if (half == 1) {
+            for (int c = 0; c < DH; ++c) EFTA_SCR[half * DH + c] = o[c];
+            const float fo = split_out_rare<D>(p, head, qt, n, row, half, viol, cs_bad, res, c1, c2, eps_mult, rs);
+            if (half == 0) fam_out = fo;
 #pragma unroll
-                for (int c = 0; c < DH; ++c) o[c] = scr[DH + c];
-            }
+            for (int c = 0; c < DH; ++c) o[c] = EFTA_SCR[half * DH + c];
         }
     }
     // store this half's columns

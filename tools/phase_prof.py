@@ -41,7 +41,7 @@ print("(the clock64 counters of the two CTAs of a pair are per-SM; compare withi
 per = np.diff(t[8:60, 0])
 print("row period median", np.median(per))
 for s_a, s_b, nm in [(9, 11, "S-issuer: issue S(j)"), (10, 12, "PV-issuer: wait P(j)"),
-                     (12, 14, "PV-issuer: wait V(j)"), (14, 13, "PV-issuer: issue PV(j)"), (13, 10, "PV-issuer: to next iter"), (1, 8, "split: ld+max+xchg+exp"), (8, 3, "split: checks+or+P st"), (3, 6, "split: to p_ready")] + [(0, 1, "wait S"), (1, 7, "tmem load S"), (7, 8, "max+exp"), (8, 9, "product check"),
+                     (12, 14, "PV-issuer: wait V(j)"), (14, 13, "PV-issuer: issue PV(j)"), (13, 10, "PV-issuer: to next iter"), (1, 8, "split: ld+max+xchg+exp"), (8, 3, "split: checks+or+P st"), (8, 5, "split: prod xchg"), (5, 7, "split: check+red.or"), (7, 3, "split: P st"), (3, 6, "split: to p_ready")] + [(0, 1, "wait S"), (1, 7, "tmem load S"), (7, 8, "max+exp"), (8, 9, "product check"),
                      (9, 15, "barrier.red.or"), (15, 2, "after or"), (2, 3, "checks+sum"), (3, 4, "P pack+store"),
                      (4, 5, "wait O(PV j-1)"), (5, 6, "correction+arrive"), (6, 0, "to next iter")]:
     dt = [(t[j, s_b] if (s_b not in (0, 10) or s_a == 9) else t[j + 1, s_b]) - t[j, s_a] for j in range(8, 60)]
