@@ -184,130 +184,16 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
     // m_run: the max P is referenced to (lazy); m_true: the running row max (reference m)
     float m_run = -CUDART_INF_F, m_true = -CUDART_INF_F, l_half = 0.0f, lb = 0.0f;
 
-    for (int j = 0; j < n; ++j) {
+    // values of block j carried from the hot loop into its tail (and the rare ladder)
+    float pv[64];
+    float bm = 0.0f, m_true_before = 0.0f, m_new = 0.0f, f = 0.0f, psum = 0.0f;
+    bool exp_affected = false;
+    int exp_viol = 0;
+    // tail of block j: P store, denominators, lazy O correction, P-ready
+    auto finish_block = [&](int j) {
         const int g = g0 + j;
         const int b = g & 1;
         const uint32_t s_addr = lane_base + L::COL_S0 + b * L::S_STRIDE;
-        const uint32_t cs_addr = s_addr + 128;
-        if (warp == 4) EFTA_TS(0, j);
-        mbar_wait(&s_full[b], (g >> 1) & 1);
-        if (warp == 4) EFTA_TS(1, j);
-        tc_fence_after();
-#ifdef EFTA_MMA_ONLY  // experiment build: tensor-pipe / operand-feed bound of the schedule
-        if (true) { split_signal_p_ready<PAIR>(&p_ready[g & 1], lane); continue; }
-#endif
-        float pv[64];
-        tmem_ld32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(&pv[0]));
-        tmem_ld32(s_addr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&pv[32]));
-        tmem_wait_ld();
-        // ---- row max: partial over this half, exchanged within the row slice
-        float mx0 = pv[0], mx1 = pv[1], mx2 = pv[2], mx3 = pv[3];
-#pragma unroll
-        for (int c = 4; c < 64; c += 4) {
-            mx0 = fmaxf(mx0, pv[c]);
-            mx1 = fmaxf(mx1, pv[c + 1]);
-            mx2 = fmaxf(mx2, pv[c + 2]);
-            mx3 = fmaxf(mx3, pv[c + 3]);
-        }
-        float* xm = xmax + b * 256;  // double-buffered by parity: the partner may still read j-1
-        xm[half * 128 + row] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-        named_bar_sync(bar_pair, 64);
-        const float mx = fmaxf(xm[row], xm[128 + row]);
-        float bm = __fmul_rn(mx, scale) + p.rowmax_bias;
-        const float m_true_before = m_true;
-        m_true = (m_true < bm) ? bm : m_true;
-        float m_new = (j == 0 || m_true - m_run > kLazyTau) ? m_true : m_run;
-        const float mL = m_new * kLog2e;
-        // ---- exponentials (MUFU + FMA-pipe polynomial), fused row sum and group products
-        const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
-        float2 ps0 = make_float2(0.0f, 0.0f), ps1 = make_float2(0.0f, 0.0f);
-        float2 prod[4];
-#pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-            const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
-            float2 e;
-            if (exp_on_fma(c)) {  // c0 is a multiple of 16: same column split as row_wg
-                e = ex2_poly2(a);
-            } else {
-                e.x = ex2_approx(a.x);
-                e.y = ex2_approx(a.y);
-            }
-            pv[c] = e.x;
-            pv[c + 1] = e.y;
-            if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
-            else ps0 = fadd2(ps0, e);
-            if (PROT) {
-                const int g = (c & 7) >> 1;
-                prod[g] = (c < kStride) ? e : fmul2(prod[g], e);
-            }
-        }
-        if (warp == 4) EFTA_TS(8, j);
-        float f = ex2_approx((m_run - m_new) * kLog2e);
-        bool exp_affected = false, factor_bad = false;
-        int exp_viol = 0;
-        if (PROT) {
-            // c1 (hi, lo) of this half's checked groups x = 4*half .. 4*half+3 (loaded after the
-            // exponentials: keeps them out of the loop's register footprint)
-            uint32_t c1h[4], c1l[4];
-            tmem_ld4(cs_addr + 4 * half, c1h);
-            tmem_ld4(cs_addr + 8 + 4 * half, c1l);
-            // hand the partner the partial products of its groups, complete our own
-            float* xp = xprod + b * 1024;
-            const float4 send = half == 0 ? make_float4(prod[2].x, prod[2].y, prod[3].x, prod[3].y)
-                                          : make_float4(prod[0].x, prod[0].y, prod[1].x, prod[1].y);
-            *reinterpret_cast<float4*>(&xp[(half * 128 + row) * 4]) = send;
-            tmem_wait_ld();
-            float pc1v[4];  // Pc1 = exp(scale*c1 - 16 m)
-            {
-                const float g16m = 16.0f * m_new;
-#pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                    const float c1 = __fadd_rn(__uint_as_float(c1h[x]), __uint_as_float(c1l[x]));
-                    pc1v[x] = ex2_approx(__fsub_rn(__fmul_rn(c1, scale), g16m) * kLog2e);
-                }
-            }
-            named_bar_sync(bar_pair, 64);
-            if (warp == 4) EFTA_TS(5, j);
-            const float4 rv = *reinterpret_cast<const float4*>(&xp[((1 - half) * 128 + row) * 4]);
-            const float2 own0 = half == 0 ? prod[0] : prod[2], own1 = half == 0 ? prod[1] : prod[3];
-            const float pr[4] = {own0.x * rv.x, own0.y * rv.y, own1.x * rv.z, own1.y * rv.w};
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-                if (!(pr[x] >= pc1v[x] * p.exp_lo && pr[x] <= pc1v[x] * p.exp_hi)) { exp_affected = true; ++exp_viol; }
-            if (!isfinite(m_new)) { exp_affected = true; exp_viol = 1; }
-            if (j > 0) factor_bad = !(f > 0.0f && f <= 1.0f);  // NaN fails both
-        }
-        float psum = (ps0.x + ps0.y) + (ps1.x + ps1.y);
-        const bool tile_trig = PROT && named_bar_or(kBarTile, 256, exp_affected || factor_bad);
-        if (warp == 4) EFTA_TS(7, j);
-        if (tile_trig) {
-            // ---- rare: exp-stage ladder + factor guard over the full rows (out of line: the
-            // row halves go through the per-SM scratch so P stays in registers here)
-#pragma unroll
-            for (int c = 0; c < 64; ++c) EFTA_SCR[half * 64 + c] = pv[c];
-#ifdef EFTA_NO_RARE_CALL
-            const float2 mb = make_float2(m_new, bm); __trap();
-#else
-            const float2 mb = split_exp_rare<D>(p, s_addr, cs_addr, head, qt, j, row, half, exp_affected, exp_viol,
-                                                m_run, m_new, bm, xpub, rs);
-#endif
-            m_new = mb.x;
-            bm = mb.y;
-            if (xpub[row * 4 + 2] != 0.0f) {
-#pragma unroll
-                for (int c = 0; c < 64; ++c) pv[c] = EFTA_SCR[half * 64 + c];
-                float2 q0 = make_float2(pv[0], pv[1]), q1 = make_float2(pv[2], pv[3]);
-#pragma unroll
-                for (int c = 4; c < 64; c += 4) {
-                    q0 = fadd2(q0, make_float2(pv[c], pv[c + 1]));
-                    q1 = fadd2(q1, make_float2(pv[c + 2], pv[c + 3]));
-                }
-                psum = (q0.x + q0.y) + (q1.x + q1.y);
-            }
-            // the recovered reference max is the row's true max so far
-            m_true = (m_true_before < m_new) ? m_new : m_true_before;
-            f = ex2_approx((m_run - m_new) * kLog2e);
-        }
         // ---- P (fp16) over this half's score columns (after the ladder: it re-reads S)
         {
             uint32_t pk[32];
@@ -353,6 +239,153 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
         split_signal_p_ready<PAIR>(&p_ready[g & 1], lane);
         if (warp == 4) EFTA_TS(6, j);
         m_run = m_new;
+    };
+    // The hot loop leaves (break) when a tile takes the rare ladder, so the out-of-line
+    // ladder call sits outside it and does not shape the loop's register allocation.
+    int j = 0;
+    for (;;) {
+        bool rare = false;
+        for (; j < n; ++j) {
+            const int g = g0 + j;
+            const int b = g & 1;
+            const uint32_t s_addr = lane_base + L::COL_S0 + b * L::S_STRIDE;
+            const uint32_t cs_addr = s_addr + 128;
+            if (warp == 4) EFTA_TS(0, j);
+            mbar_wait(&s_full[b], (g >> 1) & 1);
+            if (warp == 4) EFTA_TS(1, j);
+            tc_fence_after();
+    #ifdef EFTA_MMA_ONLY  // experiment build: tensor-pipe / operand-feed bound of the schedule
+            if (true) { split_signal_p_ready<PAIR>(&p_ready[g & 1], lane); continue; }
+    #endif
+            tmem_ld32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(&pv[0]));
+            tmem_ld32(s_addr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&pv[32]));
+            tmem_wait_ld();
+            // ---- row max: partial over this half, exchanged within the row slice
+            float mx0 = pv[0], mx1 = pv[1], mx2 = pv[2], mx3 = pv[3];
+    #pragma unroll
+            for (int c = 4; c < 64; c += 4) {
+                mx0 = fmaxf(mx0, pv[c]);
+                mx1 = fmaxf(mx1, pv[c + 1]);
+                mx2 = fmaxf(mx2, pv[c + 2]);
+                mx3 = fmaxf(mx3, pv[c + 3]);
+            }
+            float* xm = xmax + b * 256;  // double-buffered by parity: the partner may still read j-1
+            xm[half * 128 + row] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+            named_bar_sync(bar_pair, 64);
+            const float mx = fmaxf(xm[row], xm[128 + row]);
+            bm = __fmul_rn(mx, scale) + p.rowmax_bias;
+            m_true_before = m_true;
+            m_true = (m_true < bm) ? bm : m_true;
+            m_new = (j == 0 || m_true - m_run > kLazyTau) ? m_true : m_run;
+            const float mL = m_new * kLog2e;
+            // ---- exponentials (MUFU + FMA-pipe polynomial), fused row sum and group products
+            const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
+            float2 ps0 = make_float2(0.0f, 0.0f), ps1 = make_float2(0.0f, 0.0f);
+            float2 prod[4];
+    #pragma unroll
+            for (int c = 0; c < 64; c += 2) {
+                const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
+                float2 e;
+                if (exp_on_fma(c)) {  // c0 is a multiple of 16: same column split as row_wg
+                    e = ex2_poly2(a);
+                } else {
+                    e.x = ex2_approx(a.x);
+                    e.y = ex2_approx(a.y);
+                }
+                pv[c] = e.x;
+                pv[c + 1] = e.y;
+                if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
+                else ps0 = fadd2(ps0, e);
+            }
+            if (PROT) {  // strided group products of P (after the loop: fewer live registers in it)
+    #pragma unroll
+                for (int c = 0; c < 64; c += 2) {
+                    const int g = (c & 7) >> 1;
+                    const float2 e = make_float2(pv[c], pv[c + 1]);
+                    prod[g] = (c < kStride) ? e : fmul2(prod[g], e);
+                }
+            }
+            if (warp == 4) EFTA_TS(8, j);
+            f = ex2_approx((m_run - m_new) * kLog2e);
+            bool factor_bad = false;
+            exp_affected = false;
+            exp_viol = 0;
+            if (PROT) {
+                // c1 (hi, lo) of this half's checked groups x = 4*half .. 4*half+3 (loaded after the
+                // exponentials: keeps them out of the loop's register footprint)
+                uint32_t c1h[4], c1l[4];
+                tmem_ld4(cs_addr + 4 * half, c1h);
+                tmem_ld4(cs_addr + 8 + 4 * half, c1l);
+                // hand the partner the partial products of its groups, complete our own
+                float* xp = xprod + b * 1024;
+                const float4 send = half == 0 ? make_float4(prod[2].x, prod[2].y, prod[3].x, prod[3].y)
+                                              : make_float4(prod[0].x, prod[0].y, prod[1].x, prod[1].y);
+                *reinterpret_cast<float4*>(&xp[(half * 128 + row) * 4]) = send;
+                tmem_wait_ld();
+                float pc1v[4];  // Pc1 = exp(scale*c1 - 16 m)
+                {
+                    const float g16m = 16.0f * m_new;
+    #pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const float c1 = __fadd_rn(__uint_as_float(c1h[x]), __uint_as_float(c1l[x]));
+                        pc1v[x] = ex2_approx(__fsub_rn(__fmul_rn(c1, scale), g16m) * kLog2e);
+                    }
+                }
+                named_bar_sync(bar_pair, 64);
+                if (warp == 4) EFTA_TS(5, j);
+                const float4 rv = *reinterpret_cast<const float4*>(&xp[((1 - half) * 128 + row) * 4]);
+                const float2 own0 = half == 0 ? prod[0] : prod[2], own1 = half == 0 ? prod[1] : prod[3];
+                const float pr[4] = {own0.x * rv.x, own0.y * rv.y, own1.x * rv.z, own1.y * rv.w};
+    #pragma unroll
+                for (int x = 0; x < 4; ++x)
+                    if (!(pr[x] >= pc1v[x] * p.exp_lo && pr[x] <= pc1v[x] * p.exp_hi)) { exp_affected = true; ++exp_viol; }
+                if (!isfinite(m_new)) { exp_affected = true; exp_viol = 1; }
+                if (j > 0) factor_bad = !(f > 0.0f && f <= 1.0f);  // NaN fails both
+            }
+            psum = (ps0.x + ps0.y) + (ps1.x + ps1.y);
+            const bool tile_trig = PROT && named_bar_or(kBarTile, 256, exp_affected || factor_bad);
+            if (warp == 4) EFTA_TS(7, j);
+            if (tile_trig) {
+                rare = true;
+                break;
+            }
+            finish_block(j);
+        }
+        if (!rare) break;
+        {
+            const int g = g0 + j;
+            const int b = g & 1;
+            const uint32_t s_addr = lane_base + L::COL_S0 + b * L::S_STRIDE;
+            const uint32_t cs_addr = s_addr + 128;
+                // ---- rare: exp-stage ladder + factor guard over the full rows (out of line: the
+                // row halves go through the per-SM scratch so P stays in registers here)
+    #pragma unroll
+                for (int c = 0; c < 64; ++c) EFTA_SCR[half * 64 + c] = pv[c];
+    #ifdef EFTA_NO_RARE_CALL
+                const float2 mb = make_float2(m_new, bm); __trap();
+    #else
+                const float2 mb = split_exp_rare<D>(p, s_addr, cs_addr, head, qt, j, row, half, exp_affected, exp_viol,
+                                                    m_run, m_new, bm, xpub, rs);
+    #endif
+                m_new = mb.x;
+                bm = mb.y;
+                if (xpub[row * 4 + 2] != 0.0f) {
+    #pragma unroll
+                    for (int c = 0; c < 64; ++c) pv[c] = EFTA_SCR[half * 64 + c];
+                    float2 q0 = make_float2(pv[0], pv[1]), q1 = make_float2(pv[2], pv[3]);
+    #pragma unroll
+                    for (int c = 4; c < 64; c += 4) {
+                        q0 = fadd2(q0, make_float2(pv[c], pv[c + 1]));
+                        q1 = fadd2(q1, make_float2(pv[c + 2], pv[c + 3]));
+                    }
+                    psum = (q0.x + q0.y) + (q1.x + q1.y);
+                }
+                // the recovered reference max is the row's true max so far
+                m_true = (m_true_before < m_new) ? m_new : m_true_before;
+                f = ex2_approx((m_run - m_new) * kLog2e);
+        }
+        finish_block(j);
+        ++j;
     }
 
     if (next_q_row >= 0) {  // stage the next item's Q: every score MMA of this item has completed
