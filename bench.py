@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-campaign", action="store_true")
+    ap.add_argument("--no-suite", action="store_true")
     return ap.parse_args()
 
 
@@ -207,6 +208,75 @@ def fault_campaign(n_trials=20):
     return st
 
 
+def _time_cuda(fn, iters=5, warmup=2):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(iters):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def suite(dev):
+    """The other BASELINE.json configs as secondary measurements (rank 0, N=1):
+    C3 = BERT-large/GPT-2-medium attention B=16 H=16 S=2048 d=64 + the two strided-ABFT
+    FFN GEMMs (d_model 1024, d_ff 4096, 32K tokens) against cuBLAS; C5 = the full
+    FT-Transformer layer at GPT-2-large shapes over a 512..16K sequence sweep at 16K
+    tokens, protected vs the unprotected twin of the same layer."""
+    import torch
+    from paper_2504_02211_b200 import AbftLinear, EftaAttention, FTTransformerLayer, Thresholds
+    out = {}
+    thr = Thresholds(1e-4, 1e-3, 1e-3)
+    b, h, s_, d = 16, 16, 2048, 64
+    q = synth_inputs(11, (b, h, s_, d), dev)
+    k = synth_inputs(12, (b, h, s_, d), dev)
+    v = synth_inputs(13, (b, h, s_, d), dev)
+    c3 = {}
+    for mode in ("efta-opt", "none"):
+        op = EftaAttention(b, h, s_, d, mode=mode, thr=thr, device=dev)
+        ms = _time_cuda(lambda: op(q, k, v))
+        c3[f"attention_{mode}_tflops"] = round(flops(b, h, s_, d) / (ms * 1e-3) / 1e12, 2)
+    del q, k, v
+    t, dm, dff = 32768, 1024, 4096
+    g = torch.Generator(device=dev)
+    g.manual_seed(21)
+    x = (torch.empty((t, dm), device=dev).uniform_(-1, 1, generator=g)).half()
+    w1 = (torch.empty((dff, dm), device=dev).uniform_(-1, 1, generator=g) / math.sqrt(dm)).half()
+    w2 = (torch.empty((dm, dff), device=dev).uniform_(-1, 1, generator=g) / math.sqrt(dff)).half()
+    l1, l2 = AbftLinear(w1), AbftLinear(w2)
+    y1 = l1(x)
+    gf = 2.0 * t * dm * dff
+    ms_p = _time_cuda(lambda: l2(l1(x, y1)))
+    ms_u = _time_cuda(lambda: (x @ w1.t()) @ w2.t())
+    c3["ffn_abft_tflops"] = round(2 * gf / (ms_p * 1e-3) / 1e12, 2)
+    c3["ffn_cublas_tflops"] = round(2 * gf / (ms_u * 1e-3) / 1e12, 2)
+    c3["ffn_ft_overhead_pct"] = round((ms_p / ms_u - 1) * 100, 2)
+    c3["ffn_detections"] = l1.report().detections + l2.report().detections
+    out["c3"] = c3
+    del x, y1
+    c5 = []
+    lp = FTTransformerLayer(1280, 20, 5120, protect=True, thr=thr, seed=1, device=dev)
+    lu = FTTransformerLayer(1280, 20, 5120, protect=False, thr=thr, seed=1, device=dev)
+    for seq in (512, 2048, 8192, 16384):
+        bb = 16384 // seq
+        xx = (torch.empty((bb, seq, 1280), device=dev).uniform_(-1, 1, generator=g)).half()
+        ms_p = _time_cuda(lambda: lp(xx), iters=3)
+        ms_u = _time_cuda(lambda: lu(xx), iters=3)
+        fl = lp.flops(bb, seq)
+        c5.append({"seq_len": seq, "batch": bb, "protected_tflops": round(fl / (ms_p * 1e-3) / 1e12, 2),
+                   "unprotected_tflops": round(fl / (ms_u * 1e-3) / 1e12, 2),
+                   "ft_overhead_pct": round((ms_p / ms_u - 1) * 100, 2), "ms": round(ms_p, 3)})
+    out["c5_layer_sweep"] = c5
+    out["c5_detections"] = lp.report().detections
+    return out
+
+
 def ours(args):
     import torch
     rank, world, local, pg = dist_init(args.gpus)
@@ -269,7 +339,7 @@ def ours(args):
                      "frac_of_burst": round(achieved / peak_burst, 4),
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed in a "
                                     "multi-second back-to-back loop)" if peaks else "fallback",
-                     "kernel": "efta_attn_fwd_kernel<128, EFTA_OPT>",
+                     "kernel": "efta_attn_pair_kernel<128, EFTA_OPT> (persistent CTA pairs)",
                      "kernel_ms": round(ms_kern, 4), "traffic": traffic},
         "clocks": clk.result(),
         "gpu_launches": 2 * args.steps,  # checksum-encode prepass + fused attention per step
@@ -316,6 +386,11 @@ def ours(args):
             except Exception as ex:  # reported, never fatal for the perf line
                 line["fault_coverage_pct"] = None
                 line["fault_campaign"] = {"error": str(ex)[:200]}
+        if not args.no_suite:
+            try:
+                line["suite"] = suite(dev)
+            except Exception as ex:  # reported, never fatal for the perf line
+                line["suite"] = {"error": str(ex)[:200]}
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_ref()
     if rank == 0:

@@ -8,6 +8,7 @@ library exists; any compute entry point raises if the library is missing.
 _ATTN = ("EftaAttention", "FaultSpec", "FTReport", "Thresholds", "efta_forward", "validate_plan")
 _LIB = ("ConfigError", "EftaError", "SITES", "KINDS", "STATUS")
 _FFN = ("AbftLinear", "abft_gemm")
+_LAYER = ("FTTransformerLayer",)
 
 
 def __getattr__(name):
@@ -20,7 +21,10 @@ def __getattr__(name):
     if name in _FFN:
         from . import ffn
         return getattr(ffn, name)
+    if name in _LAYER:
+        from . import layer
+        return getattr(layer, name)
     raise AttributeError(name)
 
 
-__all__ = list(_ATTN + _LIB + _FFN)
+__all__ = list(_ATTN + _LIB + _FFN + _LAYER)

@@ -61,8 +61,6 @@ struct AttnParams {
     // exp-stage bracket: |ln(prod/pc1)| > eps1  <=>  prod outside [pc1*exp_lo, pc1*exp_hi]
     float exp_lo, exp_hi;
     float* scratch;  // per-SM rows for the split schedule's rare paths (kScratchSMs x 128 x 128)
-    const __half* q;   // [BH, S, D] (pair kernel: Q rows are staged into TMEM by the row warps)
-    const __half* kc;  // [BH * nblk * 32, D] strided K checksum rows (pair kernel rare path: c2)
     unsigned long long* prof;  // EFTA_PROF builds only: phase timestamps of one CTA
 };
 
@@ -70,8 +68,8 @@ struct AttnParams {
 // phase timestamps (clock64) of CTAs (2,5) and (3,5): row warp 4 lane 0 and the MMA thread
 #define EFTA_TS(slot, j)                                                                       \
     do {                                                                                       \
-        if (p.prof && (blockIdx.x == 2 || blockIdx.x == 3) && (blockIdx.y == 5 || gridDim.y == 1) && \
-            (threadIdx.x & 31) == 0 && (j) >= 0 && (j) < 64)                                               \
+        if (p.prof && (blockIdx.x == 2 || blockIdx.x == 3) && blockIdx.y == 5 &&                 \
+            (threadIdx.x & 31) == 0 && (j) < 64)                                                 \
             p.prof[(j) * 32 + (blockIdx.x & 1) * 16 + (slot)] = clock64();                       \
     } while (0)
 #else
@@ -80,10 +78,13 @@ struct AttnParams {
 
 constexpr int kScratchSMs = 256;
 
+// threads per CTA: the fast NONE / EFTA_OPT variants use the split-row schedule
+// (two row warpgroups), the tap / per-iteration-check variants one row warpgroup
+__host__ __device__ constexpr bool attn_split(int mode, bool dbg) { return false && !dbg && mode != 1; }
 // fast variants rescale O lazily (only when the running max grows by > kLazyTau)
 __host__ __device__ constexpr bool attn_lazy(int mode, bool dbg) { return !dbg && mode != 1; }
 constexpr float kLazyTau = 5.545177444479562f;  // 8 * ln 2: P <= 2^8 between rescales
-__host__ __device__ constexpr int attn_threads(int, bool) { return 256; }
+__host__ __device__ constexpr int attn_threads(int mode, bool dbg) { return attn_split(mode, dbg) ? 384 : 256; }
 
 template <int D>
 struct AttnLayout {
@@ -112,7 +113,10 @@ struct AttnLayout {
     static constexpr uint32_t OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
     static constexpr uint32_t RED_BYTES = 128 * 24 + 256;  // RowSlot[128] + ints + doubles
-    static constexpr uint32_t SMEM_BYTES = OFF_RED + RED_BYTES + 1024;  // + alignment slack
+    // split-row exchange area: xmax[2][2][128], xprod[128][16], xpub[128][4], xl[2][128] floats
+    static constexpr uint32_t OFF_XCH = OFF_RED + RED_BYTES;
+    static constexpr uint32_t XCH_BYTES = (512 + 2048 + 512 + 256) * 4;
+    static constexpr uint32_t SMEM_BYTES = OFF_XCH + XCH_BYTES + 1024;  // + alignment slack
     // TMEM: S[b] = b*160: cols 0..127 scores (P aliased over 0..63), 128..143 checksum
     // hi-products, 144..159 lo-products; O at 320: D cols + 16 hi + 16 lo checksum cols.
     static constexpr uint32_t S_STRIDE = 160;

@@ -4,8 +4,6 @@
 #include "efta_attn_pair.cuh"
 #include "efta_launch.h"
 
-#include <algorithm>
-
 #ifndef EFTA_INST_D
 #error "EFTA_INST_D must be 64 or 128"
 #endif
@@ -47,7 +45,7 @@ cudaError_t launch_d(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMa
 }
 
 template <int D, int MODE>
-cudaError_t launch_pair_t(const CUtensorMap& tka, const CUtensorMap& tkb,
+cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const CUtensorMap& tkb,
                           const CUtensorMap& tkc, const CUtensorMap& tvt, const AttnParams& p, int bh,
                           cudaStream_t st) {
     using PL = PairLayout<D, MODE != 0>;
@@ -58,16 +56,8 @@ cudaError_t launch_pair_t(const CUtensorMap& tka, const CUtensorMap& tkb,
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    // persistent: one CTA pair per TPC (two SMs), each walking (head, query-tile pair) items
-    const long long items = static_cast<long long>(p.nblk / 2) * bh;
-    const int clusters = static_cast<int>(std::min<long long>(items, nsm / 2));
-    kern<<<dim3(2 * clusters), kPairThreads, PL::SMEM_BYTES, st>>>(tka, tkb, tkc, tvt, p);
+    dim3 grid(p.nblk, bh);
+    kern<<<grid, 256, PL::SMEM_BYTES, st>>>(tq, tka, tkb, tkc, tvt, p);
     return cudaGetLastError();
 }
 
@@ -90,11 +80,11 @@ cudaError_t efta_launch_attn_d128(int mode, bool dbg, const CUtensorMap& tq, con
 #endif
 
 #if EFTA_INST_D == 64
-cudaError_t efta_launch_attn_pair_d64(int mode, const CUtensorMap& tka,
+cudaError_t efta_launch_attn_pair_d64(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                       const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
                                       const AttnParams& p, int bh, cudaStream_t st) {
-    return mode == 0 ? launch_pair_t<64, 0>(tka, tkb, tkc, tvt, p, bh, st)
-                     : launch_pair_t<64, 2>(tka, tkb, tkc, tvt, p, bh, st);
+    return mode == 0 ? launch_pair_t<64, 0>(tq, tka, tkb, tkc, tvt, p, bh, st)
+                     : launch_pair_t<64, 2>(tq, tka, tkb, tkc, tvt, p, bh, st);
 }
 cudaError_t efta_launch_encode_pair_d64(bool prot, const void* k, const void* v, void* kc, void* vt,
                                         int seq_len, int nblk, int bh, cudaStream_t st) {
@@ -108,11 +98,11 @@ cudaError_t efta_launch_encode_pair_d64(bool prot, const void* k, const void* v,
     return cudaGetLastError();
 }
 #else
-cudaError_t efta_launch_attn_pair_d128(int mode, const CUtensorMap& tka,
+cudaError_t efta_launch_attn_pair_d128(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                        const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
                                        const AttnParams& p, int bh, cudaStream_t st) {
-    return mode == 0 ? launch_pair_t<128, 0>(tka, tkb, tkc, tvt, p, bh, st)
-                     : launch_pair_t<128, 2>(tka, tkb, tkc, tvt, p, bh, st);
+    return mode == 0 ? launch_pair_t<128, 0>(tq, tka, tkb, tkc, tvt, p, bh, st)
+                     : launch_pair_t<128, 2>(tq, tka, tkb, tkc, tvt, p, bh, st);
 }
 cudaError_t efta_launch_encode_pair_d128(bool prot, const void* k, const void* v, void* kc, void* vt,
                                          int seq_len, int nblk, int bh, cudaStream_t st) {

@@ -20,25 +20,7 @@ struct RowScratch {
 // the row max state; S and its checksums are re-read from TMEM (still resident:
 // P is written over S only after this returns).
 // ----------------------------------------------------------------------------
-// c2 of the score tile for one row on the CUDA cores: scale * (Q_row . KC2_j) with
-// KC2 = c2_hi + c2_lo (rows 8..15 / 24..31 of the block's checksum rows), fp32 in
-// ascending k. Used by the pair kernel, whose score MMA carries only c1 (N = 144).
-template <int D>
-__device__ __noinline__ void pair_score_c2(const AttnParams& p, int head, int bi, int j, int row,
-                                           float (&c2s)[kStride]) {
-    const __half* qr = p.q + (static_cast<size_t>(head) * p.seq_len + static_cast<size_t>(bi) * kBlock + row) * D;
-    const __half* kc = p.kc + (static_cast<size_t>(head) * p.nblk + j) * 32 * D;
-    for (int x = 0; x < kStride; ++x) {
-        float acc = 0.0f;
-        for (int k = 0; k < D; ++k) {
-            const float w = __half2float(kc[(8 + x) * D + k]) + __half2float(kc[(24 + x) * D + k]);
-            acc = fmaf(__half2float(qr[k]), w, acc);
-        }
-        c2s[x] = __fmul_rn(acc, p.scale);
-    }
-}
-
-template <bool DBG, int PAIR_D = 0>
+template <bool DBG>
 __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr, uint32_t cs_addr,
                                             int head, int bi, int j, int row, bool exp_affected,
                                             float exp_first_residual, int exp_first_viol,
@@ -60,26 +42,15 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                 sc[c4 * 32 + x] = __fmul_rn(__uint_as_float(r[x]), p.scale);
             }
         }
-        if constexpr (PAIR_D > 0) {
-            // pair layout (N = 144): cols 0..7 c1_hi, 8..15 c1_lo; c2 on the CUDA cores
-            uint32_t q[16];
-            tmem_ld16(cs_addr, q);
-            tmem_wait_ld();
+        uint32_t qh[16], ql[16];
+        tmem_ld16(cs_addr, qh);
+        tmem_ld16(cs_addr + 16, ql);
+        tmem_wait_ld();
 #pragma unroll
-            for (int x = 0; x < kStride; ++x)
-                c1s[x] = __fmul_rn(__fadd_rn(__uint_as_float(q[x]), __uint_as_float(q[kStride + x])), p.scale);
-            pair_score_c2<PAIR_D>(p, head, bi, j, row, c2s);
-        } else {
-            uint32_t qh[16], ql[16];
-            tmem_ld16(cs_addr, qh);
-            tmem_ld16(cs_addr + 16, ql);
-            tmem_wait_ld();
-#pragma unroll
-            for (int x = 0; x < kStride; ++x) {
-                c1s[x] = __fmul_rn(__fadd_rn(__uint_as_float(qh[x]), __uint_as_float(ql[x])), p.scale);
-                c2s[x] = __fmul_rn(__fadd_rn(__uint_as_float(qh[kStride + x]), __uint_as_float(ql[kStride + x])),
-                                   p.scale);
-            }
+        for (int x = 0; x < kStride; ++x) {
+            c1s[x] = __fmul_rn(__fadd_rn(__uint_as_float(qh[x]), __uint_as_float(ql[x])), p.scale);
+            c2s[x] = __fmul_rn(__fadd_rn(__uint_as_float(qh[kStride + x]), __uint_as_float(ql[kStride + x])),
+                               p.scale);
         }
     }
     if (DBG && sc_fault_col >= 0) sc[sc_fault_col] = sc_fault_val;  // GEMM1_OUT upset lives in sc
@@ -313,6 +284,12 @@ __device__ __forceinline__ void verify_output_tile(const AttnParams& p, float (&
         push_event(p, EFTA_OUTPUT_CHECKSUM, head, bi, bj, tr.status, tr.row, tr.col, tr.violations,
                    tr.corrections, tr.checksum_repair, tr.residual, tr.delta);
 }
+
+}  // namespace efta_sm100
+
+#include "efta_attn_split.cuh"
+
+namespace efta_sm100 {
 
 
 template <bool PAIR>
@@ -808,9 +785,11 @@ template <int D, int MODE, bool DBG>
 __global__ void __launch_bounds__(attn_threads(MODE, DBG), 1)
 efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
-                     const __grid_constant__ CUtensorMap tm_vc, const __grid_constant__ AttnParams p) {
+                     const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
     using L = AttnLayout<D>;
     constexpr bool PROT = MODE != EFTA_MODE_NONE;
+    constexpr bool SPLIT = attn_split(MODE, DBG);
+    constexpr bool LAZY = attn_lazy(MODE, DBG);
     constexpr int KS = L::KS, VS = L::VS, NSUB = L::NSUB;
 
     extern __shared__ uint8_t smem_raw[];
@@ -836,7 +815,7 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         for (int s = 0; s < VS; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
         mbar_init(&s_full[0], 1);
         mbar_init(&s_full[1], 1);
-        mbar_init(p_ready, 128);
+        mbar_init(p_ready, SPLIT ? 256 : 128);
         mbar_init(o_done, 1);
         fence_barrier_init();
         tma_prefetch_desc(&tm_q);
@@ -942,7 +921,14 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
+    } else if (SPLIT && warp >= 4) {
+        RowScratch rs2;
+        rs2.slots = reinterpret_cast<RowSlot*>(smem + L::OFF_RED);
+        rs2.ints = reinterpret_cast<int*>(smem + L::OFF_RED + 128 * sizeof(RowSlot));
+        rs2.dbl = reinterpret_cast<double*>(smem + L::OFF_RED + 128 * sizeof(RowSlot) + 16 * sizeof(int));
+        row_split<D, PROT>(p, s_full, p_ready, o_done, tmem, warp, lane, head, qt, n, seq_row0, rs2,
+                           reinterpret_cast<float*>(smem + L::OFF_XCH));
+    } else if (!SPLIT && warp >= 4) {
         row_wg<D, MODE, DBG, false>(p, smem + L::OFF_RED, s_full, p_ready, o_done, tmem, warp, lane, head, qt, n, seq_row0);
     }
     tc_fence_before();

@@ -1,34 +1,20 @@
-// efta_attn_split.cuh — split-row softmax schedule of the CTA-pair EFTA kernel.
+// efta_attn_split.cuh — the "split-row" row-warpgroup schedule of the fused EFTA kernel.
 //
-// Why: with one 128-row query tile per SM and one row warpgroup, each SM
-// sub-partition runs a single softmax warp whose dependency chain (row max ->
-// 128 exponentials -> sums/products -> P store) is ~1.9x the tensor-core time of
-// the tile (tools/phase_prof.py): the MMAs idle half the time. Here two row
-// warpgroups share the tile's 128 rows (the TMEM accumulator holds all of them,
-// so no extra TMEM): warps 4-7 ("half 0") own score columns 0..63, warps 8-11
-// ("half 1") columns 64..127 of the same rows (warp w reads TMEM lanes
-// 32*(w%4)..+31). Every SM sub-partition now runs two softmax warps, each with half
-// the chain.
-//
-// Per key block j the two warps of a row slice (w, w+4) exchange through shared
-// memory, synchronised by a 64-thread named barrier private to that pair:
-//   * their partial row maxima (the reference row max, efta.cpp:150-160, is the max
-//     of the two; max is order-free so bm is bit-identical to one warpgroup's);
-//   * (protected) the partial strided products of P for the partner's groups:
-//     half 0 completes the exp-domain check of groups x = 0..3, half 1 of 4..7
-//     (snvr.cpp:52-83 as the product bracket, see efta_attn_kernel.cuh).
-// One 256-thread barrier.red.or per block decides whether the tile takes the rare
-// recovery ladder (exp_stage_slow over the full rows, run by half 0 with half 1's
-// columns handed over through a per-SM global scratch row). It sits right before
-// the P-ready arrival, where every warp has to meet the MMA issuer anyway.
-// Row sums stay per half (l = l_0 + l_1 at the end, both halves use the same lazy
-// reference max so the same factors apply). PV(j-1) is only waited for when O
-// actually has to be rescaled (lazy rescale, kLazyTau).
-//
-// Used by the fast variants (NONE / EFTA_OPTIMIZED) of efta_attn_pair_kernel; the
-// fault-tap and per-iteration-check variants keep the single-warpgroup row_wg.
+// Used by the fast variants (NONE / EFTA_OPTIMIZED, no fault taps). Two warpgroups share
+// the 128 query rows of the CTA: warps 4-7 own score columns 0..63 (and the checksum
+// columns), warps 8-11 own columns 64..127 of the same rows (same TMEM lanes: warp w reads
+// lanes 32*(w%4)..+31). Each SM sub-partition thus runs two row warps, which hides the
+// MUFU / TMEM / FMA latencies a single row warp cannot. Per key block the pair exchanges:
+//   * the partial row maxima (shared memory, one 256-thread named barrier),
+//   * (protected) warps 8-11's partial strided products of P, so warps 4-7 complete the
+//     exp-domain check of every group (second barrier) + a barrier.red.or for the tile.
+// Row sums stay per half (l = l_lo + l_hi at the end, same rescale factor f applied to
+// both). The rare recovery paths (exp-stage ladder, output correction) run on warps 4-7
+// over the full row; warps 8-11 hand over / take back their half through a per-SM global
+// scratch row (only on those paths). The numerics of every reported quantity are those of
+// the single-warpgroup schedule except the order of the max / sum reductions.
 #pragma once
-#include "efta_attn_kernel.cuh"
+#include "efta_attn.cuh"
 
 namespace efta_sm100 {
 
@@ -38,367 +24,197 @@ __device__ __forceinline__ uint32_t sm_id() {
     return r;
 }
 
-constexpr int kRowWarp0 = 3;  // first row warp of the pair kernel (warps 3..10)
+// barrier ids used by the split schedule (0 = __syncthreads, 1..7 single-warpgroup helpers)
+constexpr uint32_t kBarXmax = 8, kBarXprod = 9, kBarOr = 10, kBarRare = 11, kBarEpi = 12;
 
-// named barrier ids of the split schedule (0 = __syncthreads, 1..7 = half-0 helpers)
-constexpr uint32_t kBarPair0 = 8;   // 8..11: per row slice (warps w, w+4), 64 threads
-constexpr uint32_t kBarTile = 12;   // all 256 row threads
-constexpr uint32_t kBarRare = 13;   // all 256 row threads, rare paths
-
-// shared exchange area (floats): xmax[2][2][128] | xprod[2][2][128][4] | xpub[128][4] | xl[2][128]
-struct SplitXch {
-    static constexpr int XMAX = 0, XPROD = 512, XPUB = 512 + 2048, XL = 512 + 2048 + 512;
-    static constexpr int FLOATS = 512 + 2048 + 512 + 256;
-    static constexpr uint32_t BYTES = FLOATS * 4;
-};
-
-// Row warps: copy 128 query rows (from global row q_row0) into the TMEM A-operand columns
-// (fp16 pairs, column x = dims 2x, 2x+1); half h stages dims [D/2*h, D/2*(h+1)).
-template <int D>
-__device__ __forceinline__ void stage_q_rows(const AttnParams& p, uint32_t col_q_addr, int warp, int lane,
-                                             int q_row0) {
-    const int half = (warp - kRowWarp0) >> 2, wq = warp & 3, row = wq * 32 + lane;
-    const uint32_t lane_base = col_q_addr + (static_cast<uint32_t>(wq * 32) << 16);
-    const uint4* src = reinterpret_cast<const uint4*>(p.q + (static_cast<size_t>(q_row0) + row) * D + half * (D / 2));
-    constexpr int W = D / 4;  // 32-bit columns per half
-    uint32_t w[W];
-#pragma unroll
-    for (int i = 0; i < W / 4; ++i) {
-        const uint4 u = __ldg(src + i);
-        w[4 * i] = u.x;
-        w[4 * i + 1] = u.y;
-        w[4 * i + 2] = u.z;
-        w[4 * i + 3] = u.w;
-    }
-    if constexpr (W == 32) tmem_st32(lane_base + half * W, w);
-    else tmem_st16(lane_base + half * W, w);
-    tmem_wait_st();
-}
-
-template <bool PAIR>
-__device__ __forceinline__ void split_signal_p_ready(uint64_t* bar, int lane) {
-    __syncwarp();
-    if (lane == 0) {
-        if constexpr (PAIR) mbar_arrive_cluster(bar, 0);  // the pair leader's barrier
-        else mbar_arrive(bar);
-    }
-}
-
-// TL: TMEM plan (COL_S0, S_STRIDE, COL_O); the score checksum columns are the pair
-// layout (cols 128..135 c1_hi, 136..143 c1_lo).
-// Rare exp-stage ladder of one (i, j) tile for the split schedule: both halves have
-// dumped their 64 P values of the row into the per-SM scratch row; half 0 runs the
-// reference ladder (exp_stage_slow) over the full rows and publishes the repaired max,
-// block max and a replaced flag through xpub (P rows rewritten in the scratch).
-template <int D>
-__device__ __noinline__ float2 split_exp_rare(const AttnParams& p, uint32_t s_addr, uint32_t cs_addr, int head,
-                                              int qt, int j, int row, int half, bool exp_affected, int exp_viol,
-                                              float m_run, float m_new, float bm, float* xpub,
-                                              const RowScratch& rs) {
-    float* scr = p.scratch + static_cast<size_t>(sm_id()) * (128 * 128) + row * 128;
-    if (half == 1) {
-        xpub[row * 4 + 0] = exp_affected ? 1.0f : 0.0f;
-        xpub[row * 4 + 1] = static_cast<float>(exp_viol);
-    }
-    named_bar_sync(kBarRare, 256);
-    if (half == 0) {
-        const bool aff = exp_affected || xpub[row * 4 + 0] != 0.0f;
-        const int viol = exp_viol + static_cast<int>(xpub[row * 4 + 1]);
-        float p_loc[kBlock];
-        for (int c = 0; c < kBlock; ++c) p_loc[c] = scr[c];
-        int replaced = 0;
-        ThreadTap no_tap{};
-        exp_stage_slow<false, D>(p, s_addr, cs_addr, head, qt, j, row, aff, isfinite(m_new) ? 0.0f : CUDART_INF_F,
-                                 viol, m_run, m_new, bm, p_loc, replaced, no_tap, -1, 0.0f, rs);
-        if (replaced) {
-            for (int c = 0; c < kBlock; ++c) scr[c] = p_loc[c];
-        }
-        xpub[row * 4 + 0] = m_new;
-        xpub[row * 4 + 1] = bm;
-        xpub[row * 4 + 2] = replaced ? 1.0f : 0.0f;
-    }
-    named_bar_sync(kBarRare, 256);
-    return make_float2(xpub[row * 4 + 0], xpub[row * 4 + 1]);
-}
-
-// Rare final output correction (verify_locate_correct on O, abft.cpp:65-187) for the split
-// schedule: both halves have dumped their normalised O columns into the per-SM scratch
-// row; half 0 verifies / corrects the full rows in place and reports the tile event.
-template <int D>
-__device__ __noinline__ float split_out_rare(const AttnParams& p, int head, int qt, int n, int row, int half,
-                                             bool viol, bool cs_bad, double res, const float* c1, const float* c2,
-                                             double eps_mult, const RowScratch& rs) {
-    float* scr = p.scratch + static_cast<size_t>(sm_id()) * (128 * 128) + row * 128;
-    named_bar_sync(kBarRare, 256);
-    float fam_out = static_cast<float>(res);
-    if (half == 0) {
-        const bool tcs = named_bar_or(4, 128, cs_bad);
-        RowVerify rv{};
-        rv.best_col = -1;
-        rv.restored_col = -1;
-        rv.residual = res;
-        float full[D], cc1[kStride], cc2[kStride];
-        for (int c = 0; c < D; ++c) full[c] = scr[c];
-        for (int x = 0; x < kStride; ++x) { cc1[x] = c1[x]; cc2[x] = c2[x]; }
-        if (!tcs && viol) verify_row<D>(full, cc1, cc2, p.eps2 * eps_mult, rv);
-        for (int c = 0; c < D; ++c) scr[c] = full[c];
-        fam_out = static_cast<float>(rv.residual);
-        TileReport tr = reduce_tile_report(rv, tcs, row, rs.slots, rs.ints, rs.dbl);
-        if (row == 0)
-            push_event(p, EFTA_OUTPUT_CHECKSUM, head, qt, n, tr.status, tr.row, tr.col, tr.violations,
-                       tr.corrections, tr.checksum_repair, tr.residual, tr.delta);
-    }
-    named_bar_sync(kBarRare, 256);
-    return fam_out;
-}
-
-// One (head, query tile) work item of a persistent CTA. g0: global key-block counter of
-// this item's j = 0 (ring / barrier phases run on across items); next_q_row (>= 0): first
-// global query row of the next item, staged into TMEM once every score MMA of this item has
-// completed (so the next item's first score MMAs overlap this epilogue); o_free: arrived on once O
-// has been read out of TMEM (the next item's first P.V may overwrite it). p_ready is
-// the pair [2] indexed by block parity.
-template <int D, int MODE, bool PAIR, class TL>
+template <int D, bool PROT>
 __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full, uint64_t* p_ready,
-                                          uint64_t* o_done, uint64_t* o_free, uint32_t tmem, int warp,
-                                          int lane, int head, int qt, int n, int seq_row0, int g0,
-                                          const RowScratch& rs, float* xch, int next_q_row,
-                                          uint64_t* q_ready) {
-    using L = TL;
-    constexpr bool PROT = MODE != EFTA_MODE_NONE;
+                                          uint64_t* o_done, uint32_t tmem, int warp, int lane,
+                                          int head, int qt, int n, int seq_row0,
+                                          const RowScratch& rs, float* xch) {
+    using L = AttnLayout<D>;
     constexpr int DH = D / 2;          // O columns per half
     constexpr int GH = DH / kStride;   // output groups per half
-    const int half = (warp - kRowWarp0) >> 2;  // warp-uniform
+    const int half = (warp - 4) >> 2;  // warp-uniform
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
-    const uint32_t bar_pair = kBarPair0 + wq;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     const int c0 = half * 64;
-    float* xmax = xch + SplitXch::XMAX;
-    float* xprod = xch + SplitXch::XPROD;
-    float* xpub = xch + SplitXch::XPUB;
-    float* xl = xch + SplitXch::XL;
-    // per-SM scratch row of the rare paths (computed there: keeps the hot loop's registers free)
-#define EFTA_SCR (p.scratch + static_cast<size_t>(sm_id()) * (128 * 128) + row * 128)
+    float* xmax = xch;                // [2 parity][2 half][128]
+    float* xprod = xch + 512;         // [128][16]
+    float* xpub = xch + 512 + 2048;   // [128][4]
+    float* xl = xch + 512 + 2048 + 512;  // [2 half][128]
+    float* scr = p.scratch + static_cast<size_t>(sm_id()) * (128 * 128) + row * 128;  // rare paths
     const float scale = p.scale, scale_log2 = p.scale_log2;
-    // m_run: the max P is referenced to (lazy); m_true: the running row max (reference m)
-    float m_run = -CUDART_INF_F, m_true = -CUDART_INF_F, l_half = 0.0f, lb = 0.0f;
+    float m_run = -CUDART_INF_F, l_half = 0.0f, lb = 0.0f, fam_exp = 0.0f;
+    ThreadTap no_tap{};
 
-    // values of block j carried from the hot loop into its tail (and the rare ladder)
-    float pv[64];
-    float bm = 0.0f, m_true_before = 0.0f, m_new = 0.0f, f = 0.0f, psum = 0.0f;
-    bool exp_affected = false;
-    int exp_viol = 0;
-    // tail of block j: P store, denominators, lazy O correction, P-ready
-    auto finish_block = [&](int j) {
-        const int g = g0 + j;
-        const int b = g & 1;
+    for (int j = 0; j < n; ++j) {
+        const int b = j & 1;
         const uint32_t s_addr = lane_base + L::COL_S0 + b * L::S_STRIDE;
-        // ---- P (fp16) over this half's score columns (after the ladder: it re-reads S)
+        const uint32_t cs_addr = s_addr + 128;
+        mbar_wait(&s_full[b], (j >> 1) & 1);
+        tc_fence_after();
+        float pv[64];
+        uint32_t csr[16], csl[16];
+        tmem_ld32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(&pv[0]));
+        tmem_ld32(s_addr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&pv[32]));
+        if (PROT && half == 0) {
+            tmem_ld16(cs_addr, csr);
+            tmem_ld16(cs_addr + 16, csl);
+        }
+        tmem_wait_ld();
+        // ---- row max: partial over this half, exchanged through shared memory
+        float mx0 = pv[0], mx1 = pv[1], mx2 = pv[2], mx3 = pv[3];
+#pragma unroll
+        for (int c = 4; c < 64; c += 4) {
+            mx0 = fmaxf(mx0, pv[c]);
+            mx1 = fmaxf(mx1, pv[c + 1]);
+            mx2 = fmaxf(mx2, pv[c + 2]);
+            mx3 = fmaxf(mx3, pv[c + 3]);
+        }
+        const float pm = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+        float* xm = xmax + (j & 1) * 256;  // double-buffered: the partner may still read j-1
+        xm[half * 128 + row] = pm;
+        named_bar_sync(kBarXmax, 256);
+        const float mx = fmaxf(xm[row], xm[128 + row]);
+        float bm = __fmul_rn(mx, scale) + p.rowmax_bias;
+        float m_new = (m_run < bm) ? bm : m_run;
+        const float mL = m_new * kLog2e;
+        const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+            const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
+            pv[c] = ex2_approx(a.x);
+            pv[c + 1] = ex2_approx(a.y);
+        }
+        float f = ex2_approx((m_run - m_new) * kLog2e);
+        if (PROT) {
+            // ---- exp-domain strided product check: this half holds l = 8*half .. 8*half+7
+            float2 prod[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) prod[x] = make_float2(pv[2 * x], pv[2 * x + 1]);
+#pragma unroll
+            for (int l = 1; l < 8; ++l)
+#pragma unroll
+                for (int x = 0; x < 4; ++x)
+                    prod[x] = fmul2(prod[x], make_float2(pv[8 * l + 2 * x], pv[8 * l + 2 * x + 1]));
+            if (half == 1) {
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    xprod[row * 16 + 2 * x] = prod[x].x;
+                    xprod[row * 16 + 2 * x + 1] = prod[x].y;
+                }
+            }
+            named_bar_sync(kBarXprod, 256);
+            bool trig = false, exp_affected = false;
+            int exp_viol = 0;
+            float exp_res = 0.0f;
+            if (half == 0) {
+                const float g16m = 16.0f * m_new;
+                bool degenerate = !isfinite(m_new);
+#pragma unroll
+                for (int x = 0; x < kStride; ++x) {
+                    const float other = xprod[row * 16 + x];
+                    const float pr = ((x & 1) ? prod[x >> 1].y : prod[x >> 1].x) * other;
+                    const float c1 = __fadd_rn(__uint_as_float(csr[x]), __uint_as_float(csl[x]));
+                    const float pc1 = ex2_approx(__fsub_rn(__fmul_rn(c1, scale), g16m) * kLog2e);
+                    if (!(pr >= pc1 * p.exp_lo && pr <= pc1 * p.exp_hi)) { exp_affected = true; ++exp_viol; }
+                }
+                if (degenerate) { exp_affected = true; exp_viol = 1; exp_res = CUDART_INF_F; }
+                const bool factor_bad = j > 0 && !(f > 0.0f && f <= 1.0f);
+                trig = exp_affected || factor_bad;
+            }
+            if (named_bar_or(kBarOr, 256, trig)) {
+                // ---- rare: exp-stage ladder + factor guard over the full row on warps 4-7
+                int replaced = 0;
+                if (half == 1) {
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) scr[64 + c] = pv[c];
+                }
+                named_bar_sync(kBarRare, 256);
+                if (half == 0) {
+                    float p_loc[kBlock];
+                    for (int c = 0; c < 64; ++c) { p_loc[c] = pv[c]; p_loc[64 + c] = scr[64 + c]; }
+                    exp_stage_slow<false>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res,
+                                          exp_viol, m_run, m_new, bm, p_loc, replaced, no_tap, -1,
+                                          0.0f, rs);
+                    if (replaced) {
+                        for (int c = 0; c < 64; ++c) { pv[c] = p_loc[c]; scr[64 + c] = p_loc[64 + c]; }
+                    }
+                    xpub[row * 4 + 0] = m_new;
+                    xpub[row * 4 + 1] = bm;
+                    xpub[row * 4 + 2] = replaced ? 1.0f : 0.0f;
+                }
+                named_bar_sync(kBarRare, 256);
+                if (half == 1) {
+                    m_new = xpub[row * 4 + 0];
+                    bm = xpub[row * 4 + 1];
+                    replaced = xpub[row * 4 + 2] != 0.0f;
+                    if (replaced) {
+#pragma unroll
+                        for (int c = 0; c < 64; ++c) pv[c] = scr[64 + c];
+                    }
+                }
+                f = ex2_approx((m_run - m_new) * kLog2e);
+            }
+            if (half == 0) lb = __fadd_rn(__fmul_rn(lb, f), ex2_approx((bm - m_new) * kLog2e));
+        }
+        // ---- partial row sum, P (fp16) over this half's score columns
+        float2 ps0 = make_float2(pv[0], pv[1]), ps1 = make_float2(pv[2], pv[3]);
+#pragma unroll
+        for (int c = 4; c < 64; c += 4) {
+            ps0 = fadd2(ps0, make_float2(pv[c], pv[c + 1]));
+            ps1 = fadd2(ps1, make_float2(pv[c + 2], pv[c + 3]));
+        }
+        l_half = __fadd_rn(__fmul_rn(f, l_half), (ps0.x + ps0.y) + (ps1.x + ps1.y));
         {
             uint32_t pk[32];
 #pragma unroll
             for (int x = 0; x < 32; ++x) pk[x] = pack_half2(pv[2 * x], pv[2 * x + 1]);
             tmem_st32(s_addr + half * 32, pk);
         }
-        if (warp == 4) EFTA_TS(3, j);
-        // ---- rescale factor, lower bound, denominator (efta.cpp:192-242)
-        if (PROT) lb = __fadd_rn(__fmul_rn(lb, f), ex2_approx((bm - m_new) * kLog2e));
-        l_half = __fadd_rn(__fmul_rn(f, l_half), psum);
-        // ---- O correction: O *= f on this half's columns (+ checksum columns on half 0);
-        // only when some row of the warp moved its reference max (lazy rescale)
-        if (j > 0 && !__all_sync(0xffffffffu, f == 1.0f)) {
-            if (warp == 4) EFTA_TS(4, j);
-            mbar_wait(o_done, (g - 1) & 1);
+        // ---- O correction: each half rescales its own O columns (+ the checksum columns on half 0)
+        if (j > 0) {
+            mbar_wait(o_done, (j - 1) & 1);
             tc_fence_after();
-            constexpr int NO = DH / 32;
-            constexpr int NCH = NO + (PROT ? 1 : 0);
-            float o[NCH][32];
+            if (!__all_sync(0xffffffffu, f == 1.0f)) {
+                constexpr int NO = DH / 32;
+                float o[NO + 1][32];
 #pragma unroll
-            for (int c = 0; c < NO; ++c)
-                tmem_ld32(lane_base + L::COL_O + half * DH + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
-            if (PROT) tmem_ld16(lane_base + L::COL_O + D + half * 16, *reinterpret_cast<uint32_t(*)[16]>(&o[NO][0]));
-            tmem_wait_ld();
-            const float2 f2 = make_float2(f, f);
+                for (int c = 0; c < NO; ++c)
+                    tmem_ld32(lane_base + L::COL_O + half * DH + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
+                if (PROT && half == 0)
+                    tmem_ld32(lane_base + L::COL_O + D, *reinterpret_cast<uint32_t(*)[32]>(&o[NO][0]));
+                tmem_wait_ld();
+                const float2 f2 = make_float2(f, f);
+                const int nch = NO + ((PROT && half == 0) ? 1 : 0);
 #pragma unroll
-            for (int c = 0; c < NCH; ++c)
+                for (int c = 0; c < NO + 1; ++c) {
+                    if (c < nch) {
 #pragma unroll
-                for (int x = 0; x < 32; x += 2) {
-                    if (c == NO && x >= 16) break;
-                    const float2 r2 = fmul2(make_float2(o[c][x], o[c][x + 1]), f2);
-                    o[c][x] = r2.x;
-                    o[c][x + 1] = r2.y;
+                        for (int x = 0; x < 32; x += 2) {
+                            const float2 r2 = fmul2(make_float2(o[c][x], o[c][x + 1]), f2);
+                            o[c][x] = r2.x;
+                            o[c][x + 1] = r2.y;
+                        }
+                    }
                 }
 #pragma unroll
-            for (int c = 0; c < NO; ++c)
-                tmem_st32(lane_base + L::COL_O + half * DH + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
-            if (PROT) tmem_st16(lane_base + L::COL_O + D + half * 16, *reinterpret_cast<uint32_t(*)[16]>(&o[NO][0]));
+                for (int c = 0; c < NO; ++c)
+                    tmem_st32(lane_base + L::COL_O + half * DH + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
+                if (PROT && half == 0)
+                    tmem_st32(lane_base + L::COL_O + D, *reinterpret_cast<uint32_t(*)[32]>(&o[NO][0]));
+            }
         }
         tmem_wait_st();
         tc_fence_before();
-        split_signal_p_ready<PAIR>(&p_ready[g & 1], lane);
-        if (warp == 4) EFTA_TS(6, j);
+        mbar_arrive(p_ready);
         m_run = m_new;
-    };
-    // The hot loop leaves (break) when a tile takes the rare ladder, so the out-of-line
-    // ladder call sits outside it and does not shape the loop's register allocation.
-    int j = 0;
-    for (;;) {
-        bool rare = false;
-        for (; j < n; ++j) {
-            const int g = g0 + j;
-            const int b = g & 1;
-            const uint32_t s_addr = lane_base + L::COL_S0 + b * L::S_STRIDE;
-            const uint32_t cs_addr = s_addr + 128;
-            if (warp == 4) EFTA_TS(0, j);
-            mbar_wait(&s_full[b], (g >> 1) & 1);
-            if (warp == 4) EFTA_TS(1, j);
-            tc_fence_after();
-    #ifdef EFTA_MMA_ONLY  // experiment build: tensor-pipe / operand-feed bound of the schedule
-            if (true) { split_signal_p_ready<PAIR>(&p_ready[g & 1], lane); continue; }
-    #endif
-            tmem_ld32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(&pv[0]));
-            tmem_ld32(s_addr + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&pv[32]));
-            tmem_wait_ld();
-            // ---- row max: partial over this half, exchanged within the row slice
-            float mx0 = pv[0], mx1 = pv[1], mx2 = pv[2], mx3 = pv[3];
-    #pragma unroll
-            for (int c = 4; c < 64; c += 4) {
-                mx0 = fmaxf(mx0, pv[c]);
-                mx1 = fmaxf(mx1, pv[c + 1]);
-                mx2 = fmaxf(mx2, pv[c + 2]);
-                mx3 = fmaxf(mx3, pv[c + 3]);
-            }
-            float* xm = xmax + b * 256;  // double-buffered by parity: the partner may still read j-1
-            xm[half * 128 + row] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-            named_bar_sync(bar_pair, 64);
-            const float mx = fmaxf(xm[row], xm[128 + row]);
-            bm = __fmul_rn(mx, scale) + p.rowmax_bias;
-            m_true_before = m_true;
-            m_true = (m_true < bm) ? bm : m_true;
-            m_new = (j == 0 || m_true - m_run > kLazyTau) ? m_true : m_run;
-            const float mL = m_new * kLog2e;
-            // ---- exponentials (MUFU + FMA-pipe polynomial), fused row sum and group products
-            const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
-            float2 ps0 = make_float2(0.0f, 0.0f), ps1 = make_float2(0.0f, 0.0f);
-            float2 prod[4];
-    #pragma unroll
-            for (int c = 0; c < 64; c += 2) {
-                const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
-                float2 e;
-                if (exp_on_fma(c)) {  // c0 is a multiple of 16: same column split as row_wg
-                    e = ex2_poly2(a);
-                } else {
-                    e.x = ex2_approx(a.x);
-                    e.y = ex2_approx(a.y);
-                }
-                pv[c] = e.x;
-                pv[c + 1] = e.y;
-                if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
-                else ps0 = fadd2(ps0, e);
-            }
-            if (PROT) {  // strided group products of P (after the loop: fewer live registers in it)
-    #pragma unroll
-                for (int c = 0; c < 64; c += 2) {
-                    const int g = (c & 7) >> 1;
-                    const float2 e = make_float2(pv[c], pv[c + 1]);
-                    prod[g] = (c < kStride) ? e : fmul2(prod[g], e);
-                }
-            }
-            if (warp == 4) EFTA_TS(8, j);
-            f = ex2_approx((m_run - m_new) * kLog2e);
-            bool factor_bad = false;
-            exp_affected = false;
-            exp_viol = 0;
-            if (PROT) {
-                // c1 (hi, lo) of this half's checked groups x = 4*half .. 4*half+3 (loaded after the
-                // exponentials: keeps them out of the loop's register footprint)
-                uint32_t c1h[4], c1l[4];
-                tmem_ld4(cs_addr + 4 * half, c1h);
-                tmem_ld4(cs_addr + 8 + 4 * half, c1l);
-                // hand the partner the partial products of its groups, complete our own
-                float* xp = xprod + b * 1024;
-                const float4 send = half == 0 ? make_float4(prod[2].x, prod[2].y, prod[3].x, prod[3].y)
-                                              : make_float4(prod[0].x, prod[0].y, prod[1].x, prod[1].y);
-                *reinterpret_cast<float4*>(&xp[(half * 128 + row) * 4]) = send;
-                tmem_wait_ld();
-                float pc1v[4];  // Pc1 = exp(scale*c1 - 16 m)
-                {
-                    const float g16m = 16.0f * m_new;
-    #pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        const float c1 = __fadd_rn(__uint_as_float(c1h[x]), __uint_as_float(c1l[x]));
-                        pc1v[x] = ex2_approx(__fsub_rn(__fmul_rn(c1, scale), g16m) * kLog2e);
-                    }
-                }
-                named_bar_sync(bar_pair, 64);
-                if (warp == 4) EFTA_TS(5, j);
-                const float4 rv = *reinterpret_cast<const float4*>(&xp[((1 - half) * 128 + row) * 4]);
-                const float2 own0 = half == 0 ? prod[0] : prod[2], own1 = half == 0 ? prod[1] : prod[3];
-                const float pr[4] = {own0.x * rv.x, own0.y * rv.y, own1.x * rv.z, own1.y * rv.w};
-    #pragma unroll
-                for (int x = 0; x < 4; ++x)
-                    if (!(pr[x] >= pc1v[x] * p.exp_lo && pr[x] <= pc1v[x] * p.exp_hi)) { exp_affected = true; ++exp_viol; }
-                if (!isfinite(m_new)) { exp_affected = true; exp_viol = 1; }
-                if (j > 0) factor_bad = !(f > 0.0f && f <= 1.0f);  // NaN fails both
-            }
-            psum = (ps0.x + ps0.y) + (ps1.x + ps1.y);
-            const bool tile_trig = PROT && named_bar_or(kBarTile, 256, exp_affected || factor_bad);
-            if (warp == 4) EFTA_TS(7, j);
-            if (tile_trig) {
-                rare = true;
-                break;
-            }
-            finish_block(j);
-        }
-        if (!rare) break;
-        {
-            const int g = g0 + j;
-            const int b = g & 1;
-            const uint32_t s_addr = lane_base + L::COL_S0 + b * L::S_STRIDE;
-            const uint32_t cs_addr = s_addr + 128;
-                // ---- rare: exp-stage ladder + factor guard over the full rows (out of line: the
-                // row halves go through the per-SM scratch so P stays in registers here)
-    #pragma unroll
-                for (int c = 0; c < 64; ++c) EFTA_SCR[half * 64 + c] = pv[c];
-    #ifdef EFTA_NO_RARE_CALL
-                const float2 mb = make_float2(m_new, bm); __trap();
-    #else
-                const float2 mb = split_exp_rare<D>(p, s_addr, cs_addr, head, qt, j, row, half, exp_affected, exp_viol,
-                                                    m_run, m_new, bm, xpub, rs);
-    #endif
-                m_new = mb.x;
-                bm = mb.y;
-                if (xpub[row * 4 + 2] != 0.0f) {
-    #pragma unroll
-                    for (int c = 0; c < 64; ++c) pv[c] = EFTA_SCR[half * 64 + c];
-                    float2 q0 = make_float2(pv[0], pv[1]), q1 = make_float2(pv[2], pv[3]);
-    #pragma unroll
-                    for (int c = 4; c < 64; c += 4) {
-                        q0 = fadd2(q0, make_float2(pv[c], pv[c + 1]));
-                        q1 = fadd2(q1, make_float2(pv[c + 2], pv[c + 3]));
-                    }
-                    psum = (q0.x + q0.y) + (q1.x + q1.y);
-                }
-                // the recovered reference max is the row's true max so far
-                m_true = (m_true_before < m_new) ? m_new : m_true_before;
-                f = ex2_approx((m_run - m_new) * kLog2e);
-        }
-        finish_block(j);
-        ++j;
     }
 
-    if (next_q_row >= 0) {  // stage the next item's Q: every score MMA of this item has completed
-        stage_q_rows<D>(p, tmem + TL::COL_Q, warp, lane, next_q_row);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-            if constexpr (PAIR) mbar_arrive_cluster(q_ready, 0);
-            else mbar_arrive(q_ready);
-        }
-    }
     // ------------------------------------------------------------------ epilogue
-    mbar_wait(o_done, (g0 + n - 1) & 1);
+    mbar_wait(o_done, (n - 1) & 1);
     tc_fence_after();
     float o[DH];
     float c1[kStride], c2[kStride];
@@ -409,36 +225,15 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
         uint32_t oc[32];
         if (PROT && half == 0) tmem_ld32(lane_base + L::COL_O + D, oc);
         tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {  // O is in registers: the next item's first P.V may overwrite it
-            if constexpr (PAIR) mbar_arrive_cluster(o_free, 0);
-            else mbar_arrive(o_free);
-        }
 #pragma unroll
         for (int x = 0; x < kStride; ++x) {
             c1[x] = (PROT && half == 0) ? __fadd_rn(__uint_as_float(oc[x]), __uint_as_float(oc[16 + x])) : 0.0f;
-            c2[x] = (PROT && half == 0) ? __fadd_rn(__uint_as_float(oc[kStride + x]), __uint_as_float(oc[16 + kStride + x]))
-                                        : 0.0f;
+            c2[x] = (PROT && half == 0) ? __fadd_rn(__uint_as_float(oc[kStride + x]), __uint_as_float(oc[16 + kStride + x])) : 0.0f;
         }
     }
-    {
-        // bring O, its checksums, l and the lower bound from the lazy reference max to the
-        // row's true max (the reference's final m); F == 1 for most rows
-        const float F = ex2_approx((m_run - m_true) * kLog2e);
-        if (!__all_sync(0xffffffffu, F == 1.0f)) {
-#pragma unroll
-            for (int c = 0; c < DH; ++c) o[c] = __fmul_rn(o[c], F);
-#pragma unroll
-            for (int x = 0; x < kStride; ++x) { c1[x] = __fmul_rn(c1[x], F); c2[x] = __fmul_rn(c2[x], F); }
-            l_half = __fmul_rn(l_half, F);
-            lb = __fmul_rn(lb, F);
-        }
-        m_run = m_true;
-    }
-    // denominator: l = l_0 + l_1, then (protected) range restriction on half 0
+    // denominator: l = l_lo + l_hi, then (protected) range restriction on warps 4-7
     xl[half * 128 + row] = l_half;
-    named_bar_sync(bar_pair, 64);
+    named_bar_sync(kBarEpi, 256);
     float l_run = __fadd_rn(xl[row], xl[128 + row]);
     double eps_mult = 1.0;
     if (PROT && half == 0) {
@@ -477,14 +272,14 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
         xpub[row * 4 + 3] = l_run;
     }
     if (PROT) {
-        named_bar_sync(bar_pair, 64);
+        named_bar_sync(kBarEpi, 256);
         l_run = xpub[row * 4 + 3];
     }
 #pragma unroll
     for (int c = 0; c < DH; ++c) o[c] = __fdiv_rn(o[c], l_run);
     float fam_out = 0.0f;
     if (PROT) {
-        // final strided output check: partial group sums of this half, completed on half 0
+        // final strided output check: partial group sums of this half, completed on warps 4-7
         float s1[kStride], s2[kStride];
 #pragma unroll
         for (int x = 0; x < kStride; ++x) {
@@ -498,13 +293,11 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
             s1[x] = a;
             s2[x] = bb;
         }
-        // 16 floats per row in the row's own product-exchange slots (slice-private)
-        auto xs = [&](int k) -> float& { return xprod[(k >> 3) * 1024 + ((k >> 2) & 1) * 512 + row * 4 + (k & 3)]; };
         if (half == 1) {
 #pragma unroll
-            for (int x = 0; x < kStride; ++x) { xs(x) = s1[x]; xs(8 + x) = s2[x]; }
+            for (int x = 0; x < kStride; ++x) { xprod[row * 16 + x] = s1[x]; xprod[row * 16 + 8 + x] = s2[x]; }
         }
-        named_bar_sync(bar_pair, 64);
+        named_bar_sync(kBarEpi, 256);
         bool viol = false, cs_bad = false;
         double res = 0.0;
         if (half == 0) {
@@ -513,8 +306,8 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
                 c1[x] = __fdiv_rn(c1[x], l_run);
                 c2[x] = __fdiv_rn(c2[x], l_run);
                 cs_bad |= !isfinite(c1[x]) || !isfinite(c2[x]);
-                const float t1 = __fadd_rn(s1[x], xs(x));
-                const float t2 = __fadd_rn(s2[x], xs(8 + x));
+                const float t1 = __fadd_rn(s1[x], xprod[row * 16 + x]);
+                const float t2 = __fadd_rn(s2[x], xprod[row * 16 + 8 + x]);
                 if (!isfinite(t1) || !isfinite(t2)) { viol = true; continue; }
                 const double d1 = static_cast<double>(c1[x]) - t1;
                 const double d2 = static_cast<double>(c2[x]) - t2;
@@ -523,14 +316,34 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
             }
             fam_out = static_cast<float>(res);
         }
-        if (named_bar_or(kBarTile, 256, viol || cs_bad)) {
-            // rare: locate / correct over the full rows (out of line, rows via the scratch)
+        if (named_bar_or(kBarOr, 256, viol || cs_bad)) {
+            // rare: locate / correct over the full row on warps 4-7
+            if (half == 1) {
 #pragma unroll
-            for (int c = 0; c < DH; ++c) EFTA_SCR[half * DH + c] = o[c];
-            const float fo = split_out_rare<D>(p, head, qt, n, row, half, viol, cs_bad, res, c1, c2, eps_mult, rs);
-            if (half == 0) fam_out = fo;
+                for (int c = 0; c < DH; ++c) scr[DH + c] = o[c];
+            }
+            named_bar_sync(kBarRare, 256);
+            if (half == 0) {
+                bool tcs = named_bar_or(4, 128, cs_bad);
+                RowVerify rv{};
+                rv.best_col = -1;
+                rv.restored_col = -1;
+                rv.residual = res;
+                float full[D];
+                for (int c = 0; c < DH; ++c) { full[c] = o[c]; full[DH + c] = scr[DH + c]; }
+                if (!tcs && viol) verify_row<D>(full, c1, c2, p.eps2 * eps_mult, rv);
+                for (int c = 0; c < DH; ++c) { o[c] = full[c]; scr[DH + c] = full[DH + c]; }
+                fam_out = static_cast<float>(rv.residual);
+                TileReport tr = reduce_tile_report(rv, tcs, row, rs.slots, rs.ints, rs.dbl);
+                if (row == 0)
+                    push_event(p, EFTA_OUTPUT_CHECKSUM, head, qt, n, tr.status, tr.row, tr.col,
+                               tr.violations, tr.corrections, tr.checksum_repair, tr.residual, tr.delta);
+            }
+            named_bar_sync(kBarRare, 256);
+            if (half == 1) {
 #pragma unroll
-            for (int c = 0; c < DH; ++c) o[c] = EFTA_SCR[half * DH + c];
+                for (int c = 0; c < DH; ++c) o[c] = scr[DH + c];
+            }
         }
     }
     // store this half's columns
@@ -543,8 +356,10 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
         if (p.l_out) p.l_out[grow] = l_run;
         if (PROT) {
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1)
+            for (int off = 16; off > 0; off >>= 1) {
+                fam_exp = fmaxf(fam_exp, __shfl_xor_sync(0xffffffffu, fam_exp, off));
                 fam_out = fmaxf(fam_out, __shfl_xor_sync(0xffffffffu, fam_out, off));
+            }
             if (lane == 0) atomic_max_nonneg(&p.counters->family_max[1], fam_out);
         }
     }

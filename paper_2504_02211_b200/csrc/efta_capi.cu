@@ -198,14 +198,12 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
                                     : efta_launch_encode_pair_d128(prot, k, v, kc, r2, d->seq_len, nblk, bh, st);
             if (e != cudaSuccess) return fail(2, std::string("encode: ") + cudaGetErrorString(e));
         }
-        // K half-operands of the N = 144 (protected) / 128 score MMA: leader rows 0..71
-        // (0..63), peer rows 72..127 + the c1 hi/lo checksum rows (8-row KC boxes)
         const int vrows = prot ? D + 32 : D;
-        ok = make_map(&tk, k, rows, D, prot ? 72 : 64) &&
+        ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, rows, D, prot ? 80 : 64) &&
              make_map(&tvc, r2, static_cast<uint64_t>(bh) * nblk * vrows, 128, vrows / 2);
         if (prot)
-            ok = ok && make_map(&tv, k, rows, D, 56) &&
-                 make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 8);
+            ok = ok && make_map(&tv, k, rows, D, 48) &&
+                 make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 32);
         else {
             tv = tk;
             tkc = tk;
@@ -261,11 +259,9 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     p.scratch = wsb ? reinterpret_cast<float*>(wsb + wl.scratch) : nullptr;
     const bool dbg = d->debug != 0;
     cudaError_t e;
-    p.q = reinterpret_cast<const __half*>(q);
-    p.kc = reinterpret_cast<const __half*>(kc);
-    if (pair)  // maps: K half A, K half B (protected peer), KC, [V^T ; VC^T]; Q is staged into TMEM
-        e = (D == 64) ? efta_launch_attn_pair_d64(d->mode, tk, tv, tkc, tvc, p, bh, st)
-                      : efta_launch_attn_pair_d128(d->mode, tk, tv, tkc, tvc, p, bh, st);
+    if (pair)  // maps: q, K half A, K half B (protected peer), KC, [V^T ; VC^T]
+        e = (D == 64) ? efta_launch_attn_pair_d64(d->mode, tq, tk, tv, tkc, tvc, p, bh, st)
+                      : efta_launch_attn_pair_d128(d->mode, tq, tk, tv, tkc, tvc, p, bh, st);
     else
         e = (D == 64) ? efta_launch_attn_d64(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st)
                       : efta_launch_attn_d128(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);

@@ -20,10 +20,10 @@ void efta_internal_set_error(const char* msg);
 
 // CTA-pair (cta_group::2) fast path: modes NONE / EFTA_OPT, even number of query tiles.
 // maps: q, k half A, k half B (protected peer), kc, [V^T; VC^T].
-cudaError_t efta_launch_attn_pair_d64(int mode, const CUtensorMap& tka,
+cudaError_t efta_launch_attn_pair_d64(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                       const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
                                       const efta_sm100::AttnParams& p, int bh, cudaStream_t st);
-cudaError_t efta_launch_attn_pair_d128(int mode, const CUtensorMap& tka,
+cudaError_t efta_launch_attn_pair_d128(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                        const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
                                        const efta_sm100::AttnParams& p, int bh, cudaStream_t st);
 cudaError_t efta_launch_encode_pair_d64(bool prot, const void* k, const void* v, void* kc, void* vt,

@@ -1,0 +1,93 @@
+"""FT-Transformer layer (arXiv 2504.02211 Fig. 1 / SURVEY.md §8(f) F1): every linear module
+through the strided-ABFT tcgen05 GEMM, attention through the fused EFTA kernel.
+
+    layer = FTTransformerLayer(d_model=1280, n_heads=20, d_ff=5120)   # GPT-2-large shapes
+    y = layer(x)                  # x: CUDA fp16 [batch, seq, d_model] -> y fp16
+    rep = layer.report()          # merged FT outcome of the 4 GEMMs + attention
+
+Structure (the paper applies strided ABFT to "all linear modules"):
+    qkv = X Wqkv^T      (AbftLinear, N = 3 d_model)
+    O   = EFTA(Q, K, V) (EftaAttention, EFTA-optimized)
+    h   = X + O Wo^T    (AbftLinear)
+    y   = h + GELU(h W1^T) W2^T   (AbftLinear x 2)
+The head split / merge and the GELU / residual adds are torch element-wise plumbing between
+the protected kernels (no normalisation layers: the reference protects only the GEMMs and
+the attention). `protect=False` builds the unprotected twin of the same layer (cuBLAS
+linears, the same attention kernel in mode NONE) for the FT-overhead comparison.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .attention import EftaAttention, FTReport, Thresholds
+from .ffn import AbftLinear
+
+
+def _weight(n, k, gen, device):
+    w = torch.empty((n, k), dtype=torch.float32, device=device).uniform_(-1.0, 1.0, generator=gen)
+    return (w / math.sqrt(k)).to(torch.float16)
+
+
+class FTTransformerLayer:
+    def __init__(self, d_model=1280, n_heads=20, d_ff=5120, protect=True, thr=None, gemm_eps=1e-2,
+                 seed=0, device="cuda"):
+        if d_model % n_heads:
+            raise ValueError("d_model must be a multiple of n_heads")
+        self.d_model, self.n_heads, self.d_ff = d_model, n_heads, d_ff
+        self.head_dim = d_model // n_heads
+        self.protect = protect
+        self.thr = thr or Thresholds(1e-4, 1e-3, 1e-3)
+        gen = torch.Generator(device=device)
+        gen.manual_seed(seed)
+        self.w = {name: _weight(n, k, gen, device)
+                  for name, (n, k) in (("qkv", (3 * d_model, d_model)), ("o", (d_model, d_model)),
+                                       ("ff1", (d_ff, d_model)), ("ff2", (d_model, d_ff)))}
+        self.lin = {name: AbftLinear(w, eps=gemm_eps) for name, w in self.w.items()} if protect else None
+        self._attn = {}
+
+    def _linear(self, name, x):
+        if self.protect:
+            return self.lin[name](x)
+        return x @ self.w[name].t()
+
+    def _attention(self, b, s):
+        key = (b, s)
+        if key not in self._attn:
+            self._attn[key] = EftaAttention(b, self.n_heads, s, self.head_dim,
+                                            mode="efta-opt" if self.protect else "none", thr=self.thr,
+                                            device=self.w["o"].device)
+        return self._attn[key]
+
+    def flops(self, b, s):
+        t = b * s
+        lin = 2.0 * t * (4 * self.d_model * self.d_model + 2 * self.d_model * self.d_ff)
+        return lin + 4.0 * b * self.n_heads * s * s * self.head_dim
+
+    def __call__(self, x: torch.Tensor) -> torch.Tensor:
+        b, s, d = x.shape
+        t = b * s
+        x2 = x.reshape(t, d)
+        qkv = self._linear("qkv", x2)                                   # [t, 3d]
+        qkv = qkv.view(b, s, 3, self.n_heads, self.head_dim).permute(2, 0, 3, 1, 4).contiguous()
+        attn = self._attention(b, s)
+        o, _, _ = attn(qkv[0], qkv[1], qkv[2])                          # [b, h, s, dh] fp32
+        o = o.to(torch.float16).permute(0, 2, 1, 3).reshape(t, d)
+        h = x2 + self._linear("o", o)
+        f = self._linear("ff2", torch.nn.functional.gelu(self._linear("ff1", h)))
+        return (h + f).view(b, s, d)
+
+    def report(self) -> FTReport:
+        rep = FTReport(mode="layer")
+        parts = [a.report() for a in self._attn.values()]
+        if self.protect:
+            parts += [lin.report() for lin in self.lin.values()]
+        for r in parts:
+            rep.events += r.events
+            rep.detections += r.detections
+            rep.corrections += r.corrections
+            rep.recomputes += r.recomputes
+            rep.range_replacements += r.range_replacements
+            rep.failed = rep.failed or r.failed
+        return rep
