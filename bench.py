@@ -339,7 +339,7 @@ def ours(args):
                      "frac_of_burst": round(achieved / peak_burst, 4),
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed in a "
                                     "multi-second back-to-back loop)" if peaks else "fallback",
-                     "kernel": "efta_attn_pair_kernel<128, EFTA_OPT> (persistent CTA pairs)",
+                     "kernel": "efta_attn_pair_kernel<128, EFTA_OPT> (CTA pairs, two alternating row warpgroups)",
                      "kernel_ms": round(ms_kern, 4), "traffic": traffic},
         "clocks": clk.result(),
         "gpu_launches": 2 * args.steps,  # checksum-encode prepass + fused attention per step

@@ -62,6 +62,8 @@ struct AttnParams {
     float exp_lo, exp_hi;
     float* scratch;  // per-SM rows for the split schedule's rare paths (kScratchSMs x 128 x 128)
     unsigned long long* prof;  // EFTA_PROF builds only: phase timestamps of one CTA
+    const __half* q;           // [BH, S, D]: the pair kernel's rare path recomputes score c2 from Q . KC2
+    const __half* kc;          // [BH*n, 32, D] checksum rows (workspace)
 };
 
 #ifdef EFTA_PROF
@@ -69,7 +71,7 @@ struct AttnParams {
 #define EFTA_TS(slot, j)                                                                       \
     do {                                                                                       \
         if (p.prof && (blockIdx.x == 2 || blockIdx.x == 3) && blockIdx.y == 5 &&                 \
-            (threadIdx.x & 31) == 0 && (j) < 64)                                                 \
+            (threadIdx.x & 31) == 0 && (j) >= 0 && (j) < 64)                                               \
             p.prof[(j) * 32 + (blockIdx.x & 1) * 16 + (slot)] = clock64();                       \
     } while (0)
 #else
@@ -288,18 +290,20 @@ struct RowSlot {
     int best_col, restored_col;
 };
 
-__device__ __forceinline__ void wg_sync() { named_bar_sync(1, 128); }
+// bo: barrier-id offset of the calling row warpgroup (0, or kBarAltOfs for the second
+// warpgroup of the alternating schedule, efta_attn_alt.cuh)
+__device__ __forceinline__ void wg_sync(uint32_t bo = 0) { named_bar_sync(1 + bo, 128); }
 
 // All 128 row threads call this; returns the tile report on thread 0 (row 0).
 static __device__ __noinline__ TileReport reduce_tile_report(const RowVerify& rv, bool tile_nonfinite,
                                                      int row, RowSlot* slots, int* ints,
-                                                     double* dbl) {
+                                                     double* dbl, uint32_t bo = 0) {
     // ints: [0] violations [1] corrections [2] checksum_repair [3] uncorrectable [4] nonfinite
     if (row == 0) {
         for (int i = 0; i < 5; ++i) ints[i] = 0;
         dbl[0] = 0.0;
     }
-    wg_sync();
+    wg_sync(bo);
     atomicAdd(&ints[0], rv.violations);
     atomicAdd(&ints[1], rv.corrections);
     if (rv.checksum_repair) atomicOr(&ints[2], 1);
@@ -319,7 +323,7 @@ static __device__ __noinline__ TileReport reduce_tile_report(const RowVerify& rv
             old = atomicCAS(a, assumed, __double_as_longlong(rv.residual));
         } while (old != assumed);
     }
-    wg_sync();
+    wg_sync(bo);
     TileReport tr{};
     if (row == 0) {
         tr.violations = ints[0];
@@ -359,7 +363,7 @@ static __device__ __noinline__ TileReport reduce_tile_report(const RowVerify& rv
             else tr.status = EFTA_CLEAN;
         }
     }
-    wg_sync();
+    wg_sync(bo);
     return tr;
 }
 

@@ -1,0 +1,386 @@
+// efta_attn_alt.cuh — alternating row-warpgroup schedule of the CTA-pair EFTA kernel.
+//
+// Why: with one row warpgroup, each SM sub-partition runs a single softmax warp whose
+// chain per key block (TMEM load -> max -> 128 exponentials + strided products -> check
+// -> P store) is ~2.1x the tensor-core time of the block (tools/phase_prof.py: row period
+// 2729 clk protected vs 1280 clk of MMAs): the MMAs idle half the time and the warp
+// itself is latency-bound (issue-active ~37%).
+//
+// Here two row warpgroups own ALTERNATE key blocks of the same 128 query rows:
+// warpgroup w (warps 4+4w .. 7+4w) processes blocks j = w, w+2, ... from S buffer w
+// (the S accumulator is already double-buffered by block parity, so no extra TMEM).
+// Each sub-partition now runs two independent softmax warps. The online-softmax
+// recurrence (src/efta.cpp:192-260) couples consecutive blocks only through the row
+// maxima; those are handed from one warpgroup to the other through shared memory:
+//   * early: right after its row max, warpgroup w publishes (m_true, m_run) of block j
+//     (the running true max and the lazy reference max P is computed against), so the
+//     partner's block j+1 can start its exponentials;
+//   * late: after its tile decision (exp-stage check, factor guard and, on a violation,
+//     the recovery ladder exp_stage_slow that may repair the max), it publishes the
+//     final values. The partner compares them with the early ones it used at the same
+//     point of its own block; on a mismatch (only possible after a recovery changed a
+//     max) it recomputes its block from the still-resident S with the revised values,
+//     which reproduces the sequential recurrence exactly.
+// Row sums l and the range lower bound lb are kept per warpgroup, each referenced to
+// the warpgroup's own last reference max, and merged at the end
+// (l = l_0 e^{m_0 - m} + l_1 e^{m_1 - m}). O is one TMEM accumulator for both; it is
+// rescaled (lazily, kLazyTau) by the warpgroup whose block moved the reference max,
+// after P.V of the previous block completed.
+//
+// Barriers: per warpgroup a P-ready barrier (4 warps x 2 CTAs), per (warpgroup, warp
+// quarter) an early and a late chain barrier (32 arrivals). Named barriers: warpgroup 0
+// uses the single-warpgroup ids 1..7, warpgroup 1 the same + kBarAltOfs (9, 10, 11, 14),
+// id 8 hands warpgroup 1's sums to warpgroup 0, which alone runs the epilogue.
+#pragma once
+#include "efta_attn_kernel.cuh"
+// included by efta_attn_pair.cuh after PairLayout
+
+namespace efta_sm100 {
+
+constexpr uint32_t kBarAltFin = 8;
+constexpr uint32_t kBarAltOfs = 8;
+
+struct AltXch {
+    float2 early[2][128];  // (m_true, m_run) of the producer warpgroup's last block, fast path
+    float2 late[2][128];   // the same after the producer's tile decision / recovery
+    float4 fin[128];       // warpgroup 1 -> 0 after the loop: l, lb, m_ref, m_true
+};
+static_assert(sizeof(AltXch) == 6144, "PairLayout reserves 6 KB for the chain exchange");
+
+template <int D, bool PROT>
+__device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, uint64_t* s_full,
+                                        uint64_t* s_free, uint64_t* p_ready, uint64_t* o_done, uint64_t* o_final,
+                                        uint64_t* mx_early, uint64_t* mx_late, uint32_t tmem, int warp,
+                                        int lane, int head, int qt, int n, int seq_row0) {
+    using L = PairLayout<D, PROT>;
+    constexpr int MODE = PROT ? EFTA_MODE_EFTA_OPT : EFTA_MODE_NONE;
+    const int w = (warp - 4) >> 2;
+    const int wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t bo = w ? kBarAltOfs : 0u;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    RowScratch rs;
+    {
+        uint8_t* r = red + w * L::RED_BYTES;
+        rs.slots = reinterpret_cast<RowSlot*>(r);
+        rs.ints = reinterpret_cast<int*>(r + 128 * sizeof(RowSlot));
+        rs.dbl = reinterpret_cast<double*>(r + 128 * sizeof(RowSlot) + 16 * sizeof(int));
+    }
+    ThreadTap tap{};  // inactive: the tap variants run the single-warpgroup kernel
+    uint64_t* my_early = mx_early + w * 4 + wq;
+    uint64_t* my_late = mx_late + w * 4 + wq;
+    uint64_t* pa_early = mx_early + (1 - w) * 4 + wq;
+    uint64_t* pa_late = mx_late + (1 - w) * 4 + wq;
+    const float scale = p.scale, scale_log2 = p.scale_log2;
+    // own sums, referenced to m_ref (the reference max of this warpgroup's last block)
+    float l_w = 0.0f, lb_w = 0.0f, m_ref = -CUDART_INF_F, m_true_last = -CUDART_INF_F;
+    const uint32_t s_addr = lane_base + L::COL_S0 + w * L::SW;
+    const uint32_t cs_addr = s_addr + 128;  // c1_hi (8) | c1_lo (8)
+
+    int it = 0;
+    for (int j = w; j < n; j += 2, ++it) {
+        if ((warp & 3) == 0) EFTA_TS(0, j);
+        mbar_wait(&s_full[w], it & 1);
+        if ((warp & 3) == 0) EFTA_TS(1, j);
+        tc_fence_after();
+        const uint32_t pph = static_cast<uint32_t>((j - 1) >> 1) & 1u;  // partner's phase for block j-1
+        float pv[kBlock];
+        float m_true_prev = -CUDART_INF_F, m_run_prev = -CUDART_INF_F;
+        float m_true, m_new, bm, psum_f = 0.0f;
+        bool replaced_p = false;
+        for (int attempt = 0;; ++attempt) {
+            uint32_t csr[16];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4)
+                tmem_ld32(s_addr + c4 * 32, *reinterpret_cast<uint32_t(*)[32]>(&pv[c4 * 32]));
+            if (PROT) tmem_ld16(cs_addr, csr);
+            tmem_wait_ld();
+            if (PROT) {
+#pragma unroll
+                for (int x = 0; x < kStride; ++x)
+                    csr[x] = __float_as_uint(__fadd_rn(__uint_as_float(csr[x]), __uint_as_float(csr[kStride + x])));
+            }
+            float mx0 = pv[0], mx1 = pv[1], mx2 = pv[2], mx3 = pv[3];
+#pragma unroll
+            for (int c = 4; c < kBlock; c += 4) {
+                mx0 = fmaxf(mx0, pv[c]);
+                mx1 = fmaxf(mx1, pv[c + 1]);
+                mx2 = fmaxf(mx2, pv[c + 2]);
+                mx3 = fmaxf(mx3, pv[c + 3]);
+            }
+            bm = __fmul_rn(fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)), scale) + p.rowmax_bias;
+            // ---- the max chain: block j-1 belongs to the partner warpgroup
+            if (j > 0) {
+                if (attempt == 0) {
+                    mbar_wait(pa_early, pph);
+                    const float2 c = xc->early[1 - w][row];
+                    m_true_prev = c.x;
+                    m_run_prev = c.y;
+                } else {
+                    const float2 c = xc->late[1 - w][row];
+                    m_true_prev = c.x;
+                    m_run_prev = c.y;
+                }
+            }
+            m_true = (m_true_prev < bm) ? bm : m_true_prev;
+            m_new = (j == 0 || m_true - m_run_prev > kLazyTau) ? m_true : m_run_prev;
+            if (attempt == 0) {
+                xc->early[w][row] = make_float2(m_true, m_new);
+                mbar_arrive(my_early);
+            }
+            const float mL = m_new * kLog2e;
+            float pc1v[kStride];
+            float2 prod_f[kStride / 2];
+            if (PROT) {
+                const float g16m = 16.0f * m_new;
+#pragma unroll
+                for (int x = 0; x < kStride; ++x)
+                    pc1v[x] = ex2_approx(__fsub_rn(__fmul_rn(__uint_as_float(csr[x]), scale), g16m) * kLog2e);
+            }
+            const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
+            float2 ps0 = make_float2(0.0f, 0.0f), ps1 = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int c = 0; c < kBlock; c += 2) {
+                const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
+                float2 e;
+                if (exp_on_fma(c)) {
+                    e = ex2_poly2(a);
+                } else {
+                    e.x = ex2_approx(a.x);
+                    e.y = ex2_approx(a.y);
+                }
+                pv[c] = e.x;
+                pv[c + 1] = e.y;
+                if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
+                else ps0 = fadd2(ps0, e);
+                if (PROT) {
+                    const int g = (c & 7) >> 1;
+                    prod_f[g] = (c < kStride) ? e : fmul2(prod_f[g], e);
+                }
+            }
+            psum_f = (ps0.x + ps0.y) + (ps1.x + ps1.y);
+            if (!PROT) break;  // no recovery path: the chain can never be revised
+
+            // ---- exp-domain strided product check (see row_wg) + factor guard
+            const float f = ex2_approx((m_run_prev - m_new) * kLog2e);
+            bool exp_affected = false;
+            int exp_viol = 0;
+            bool degenerate = !isfinite(m_new);
+#pragma unroll
+            for (int x = 0; x < kStride; ++x) {
+                const float pr = (x & 1) ? prod_f[x >> 1].y : prod_f[x >> 1].x;
+                const bool bad = !(pr >= pc1v[x] * p.exp_lo && pr <= pc1v[x] * p.exp_hi);
+                if (bad) { exp_affected = true; ++exp_viol; }
+            }
+            float exp_res = 0.0f;
+            if (degenerate) { exp_affected = true; exp_res = CUDART_INF_F; exp_viol = 1; }
+            const bool factor_bad = (j > 0) && !(f > 0.0f && f <= 1.0f);
+            // ---- late chain check: did the partner's decision revise block j-1's maxima?
+            bool chain_bad = false;
+            if (j > 0) {
+                if (attempt == 0) mbar_wait(pa_late, pph);
+                const float2 c = xc->late[1 - w][row];
+                chain_bad = __float_as_uint(c.x) != __float_as_uint(m_true_prev) ||
+                            __float_as_uint(c.y) != __float_as_uint(m_run_prev);
+            }
+            if ((warp & 3) == 0) EFTA_TS(9, j);
+            if (!named_bar_or(6 + bo, 128, exp_affected || factor_bad || chain_bad)) break;
+            if (named_bar_or(6 + bo, 128, chain_bad)) continue;  // redo the block with the revised maxima
+            // ---- rare: the reference recovery ladder for this tile
+            float p_loc[kBlock];
+#pragma unroll
+            for (int c = 0; c < kBlock; ++c) p_loc[c] = pv[c];
+            int replaced = 0;
+            exp_stage_slow<false, D>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res, exp_viol,
+                                  m_run_prev, m_new, bm, p_loc, replaced, tap, -1, 0.0f, rs, bo);
+            if (replaced) {
+#pragma unroll
+                for (int c = 0; c < kBlock; ++c) pv[c] = p_loc[c];
+            }
+            replaced_p = replaced != 0;
+            m_true = (m_true_prev < m_new) ? m_new : m_true_prev;
+            break;
+        }
+        if (PROT) {
+            xc->late[w][row] = make_float2(m_true, m_new);
+            mbar_arrive(my_late);
+        }
+        // S_j is no longer read: the score MMA of block j+2 may overwrite S[w]
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&s_free[w], 0);
+        if ((warp & 3) == 0) EFTA_TS(2, j);
+        // ---- factors: fo for the shared O accumulator (chain), fw for this warpgroup's sums
+        const float fo = ex2_approx((m_run_prev - m_new) * kLog2e);
+        const float fw = ex2_approx((m_ref - m_new) * kLog2e);
+        if (PROT) lb_w = __fadd_rn(__fmul_rn(lb_w, fw), ex2_approx((bm - m_new) * kLog2e));
+        float psum = psum_f;
+        if (replaced_p) {
+            float2 ps0 = make_float2(pv[0], pv[1]), ps1 = make_float2(pv[2], pv[3]);
+#pragma unroll
+            for (int c = 4; c < kBlock; c += 4) {
+                ps0 = fadd2(ps0, make_float2(pv[c], pv[c + 1]));
+                ps1 = fadd2(ps1, make_float2(pv[c + 2], pv[c + 3]));
+            }
+            psum = (ps0.x + ps0.y) + (ps1.x + ps1.y);
+        }
+        l_w = __fadd_rn(__fmul_rn(fw, l_w), psum);
+
+        if ((warp & 3) == 0) EFTA_TS(3, j);
+        // ---- P (fp16) into the shared P buffer, once P.V of block j-1 has consumed it
+        if (j > 0) {
+            if ((warp & 3) == 0) EFTA_TS(4, j);
+            mbar_wait(&o_done[1 - w], static_cast<uint32_t>((j - 1) >> 1) & 1u);
+            if ((warp & 3) == 0) EFTA_TS(5, j);
+            tc_fence_after();
+        }
+        {
+            uint32_t pk[32];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int x = 0; x < 32; ++x) pk[x] = pack_half2(pv[h * 64 + 2 * x], pv[h * 64 + 2 * x + 1]);
+                tmem_st32(lane_base + L::COL_P + h * 32, pk);
+            }
+        }
+        // ---- O *= fo (lazy: only when this block moved the reference max of some row);
+        // P.V of block j-1 is complete (waited above)
+        if (j > 0 && !__all_sync(0xffffffffu, fo == 1.0f)) {
+            constexpr int NCH = D / 32 + (PROT ? 1 : 0);
+            float o[NCH][32];
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+                tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
+            tmem_wait_ld();
+            const float2 f2 = make_float2(fo, fo);
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                for (int x = 0; x < 32; x += 2) {
+                    const float2 r2 = fmul2(make_float2(o[c][x], o[c][x + 1]), f2);
+                    o[c][x] = r2.x;
+                    o[c][x + 1] = r2.y;
+                }
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+                tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        signal_p_ready<true>(&p_ready[w], lane);
+        if ((warp & 3) == 0) EFTA_TS(6, j);
+        m_ref = m_new;
+        m_true_last = m_true;
+    }
+
+    // ------------------------------------------------ hand-over: warpgroup 1 -> 0
+    if (w == 1) {
+        xc->fin[row] = make_float4(l_w, lb_w, m_ref, m_true_last);
+        named_bar_arrive(kBarAltFin, 256);
+        return;
+    }
+    named_bar_sync(kBarAltFin, 256);
+    const float4 fb = xc->fin[row];
+    const bool last_b = ((n - 1) & 1) != 0;
+    float m_run = last_b ? fb.z : m_ref;           // the chain's final reference max
+    const float m_true = last_b ? fb.w : m_true_last;
+    const float fa = ex2_approx((m_ref - m_run) * kLog2e);
+    const float fbf = ex2_approx((fb.z - m_run) * kLog2e);
+    float l_run = __fadd_rn(__fmul_rn(l_w, fa), __fmul_rn(fb.x, fbf));
+    float lb = __fadd_rn(__fmul_rn(lb_w, fa), __fmul_rn(fb.y, fbf));
+
+    // ------------------------------------------------ epilogue (as row_wg, warpgroup 0 only)
+    mbar_wait(o_final, 0);
+    tc_fence_after();
+    float o[D];
+    float c1[kStride], c2[kStride];
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c)
+        tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
+    {
+        uint32_t oc[32];
+        if (PROT) tmem_ld32(lane_base + L::COL_O + D, oc);
+        tmem_wait_ld();
+#pragma unroll
+        for (int x = 0; x < kStride; ++x) {
+            c1[x] = PROT ? __fadd_rn(__uint_as_float(oc[x]), __uint_as_float(oc[16 + x])) : 0.0f;
+            c2[x] = PROT ? __fadd_rn(__uint_as_float(oc[kStride + x]), __uint_as_float(oc[16 + kStride + x]))
+                         : 0.0f;
+        }
+    }
+    {
+        // bring O, its checksums, l and the lower bound from the lazy reference max to
+        // the row's true max (the reference's final m); F == 1 for most rows
+        const float F = ex2_approx((m_run - m_true) * kLog2e);
+        if (!__all_sync(0xffffffffu, F == 1.0f)) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) o[c] = __fmul_rn(o[c], F);
+#pragma unroll
+            for (int x = 0; x < kStride; ++x) { c1[x] = __fmul_rn(c1[x], F); c2[x] = __fmul_rn(c2[x], F); }
+            l_run = __fmul_rn(l_run, F);
+            lb = __fmul_rn(lb, F);
+        }
+        m_run = m_true;
+    }
+    float fam_out = 0.0f;
+    double eps_mult = 1.0;
+    if (PROT) {
+        // denominator range restriction (snvr.cpp:161-182, efta.cpp:289-310)
+        const float upper = static_cast<float>(p.seq_len);
+        const bool bad = !isfinite(l_run) || l_run < lb || l_run > upper;
+        double viol = 0.0;
+        if (bad) {
+            viol = !isfinite(l_run) ? CUDART_INF
+                                    : (l_run < lb ? static_cast<double>(lb) - l_run
+                                                  : static_cast<double>(l_run) - upper);
+            l_run = lb;
+            eps_mult = static_cast<double>(p.seq_len) / static_cast<double>(l_run);
+        }
+        if (named_bar_or(7, 128, bad)) {
+            if (row == 0) { rs.ints[0] = 0; rs.ints[1] = 0x7fffffff; rs.dbl[0] = 0.0; }
+            wg_sync();
+            if (bad) {
+                atomicAdd(&rs.ints[0], 1);
+                atomicMin(&rs.ints[1], row);
+                unsigned long long* a = reinterpret_cast<unsigned long long*>(&rs.dbl[0]);
+                unsigned long long old = *a, assumed;
+                do {
+                    assumed = old;
+                    if (__longlong_as_double(assumed) >= viol) break;
+                    old = atomicCAS(a, assumed, __double_as_longlong(viol));
+                } while (old != assumed);
+            }
+            wg_sync();
+            if (row == 0) {
+                atomicAdd(&p.counters->range_replacements, rs.ints[0]);
+                push_event(p, EFTA_ROWSUM_RANGE, head, qt, n, EFTA_CORRECTED, rs.ints[1], -1, 0, rs.ints[0], 0,
+                           rs.dbl[0], 0.0);
+            }
+            wg_sync();
+        }
+    }
+    // normalization (efta.cpp:312-327)
+#pragma unroll
+    for (int c = 0; c < D; ++c) o[c] = __fdiv_rn(o[c], l_run);
+    if (PROT) {
+#pragma unroll
+        for (int x = 0; x < kStride; ++x) { c1[x] = __fdiv_rn(c1[x], l_run); c2[x] = __fdiv_rn(c2[x], l_run); }
+        float res;
+        verify_output_tile<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res);
+        if (isfinite(res)) fam_out = fmaxf(fam_out, res);
+    }
+    const size_t grow = static_cast<size_t>(seq_row0) + qt * kBlock + row;
+    float4* dst = reinterpret_cast<float4*>(p.o + grow * D);
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+    if (p.m_out) p.m_out[grow] = m_run;
+    if (p.l_out) p.l_out[grow] = l_run;
+    if (PROT) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) fam_out = fmaxf(fam_out, __shfl_xor_sync(0xffffffffu, fam_out, off));
+        if (lane == 0) atomic_max_nonneg(&p.counters->family_max[1], fam_out);
+    }
+    (void)MODE;
+}
+
+}  // namespace efta_sm100

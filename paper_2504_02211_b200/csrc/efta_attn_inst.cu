@@ -57,7 +57,7 @@ cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const C
         attr_set = true;
     }
     dim3 grid(p.nblk, bh);
-    kern<<<grid, 256, PL::SMEM_BYTES, st>>>(tq, tka, tkb, tkc, tvt, p);
+    kern<<<grid, kPairThreads, PL::SMEM_BYTES, st>>>(tq, tka, tkb, tkc, tvt, p);
     return cudaGetLastError();
 }
 

@@ -20,14 +20,34 @@ struct RowScratch {
 // the row max state; S and its checksums are re-read from TMEM (still resident:
 // P is written over S only after this returns).
 // ----------------------------------------------------------------------------
-template <bool DBG>
+// c2 of the score tile for one row on the CUDA cores: scale * (Q_row . KC2_j) with
+// KC2 = c2_hi + c2_lo (rows 8..15 / 24..31 of the block's checksum rows), fp32 in
+// ascending k. Used by the pair kernel, whose score MMA carries only c1 (N = 144).
+template <int D>
+__device__ __noinline__ void pair_score_c2(const AttnParams& p, int head, int bi, int j, int row,
+                                           float (&c2s)[kStride]) {
+    const __half* qr = p.q + (static_cast<size_t>(head) * p.seq_len + static_cast<size_t>(bi) * kBlock + row) * D;
+    const __half* kc = p.kc + (static_cast<size_t>(head) * p.nblk + j) * 32 * D;
+    for (int x = 0; x < kStride; ++x) {
+        float acc = 0.0f;
+        for (int k = 0; k < D; ++k) {
+            const float w = __half2float(kc[(8 + x) * D + k]) + __half2float(kc[(24 + x) * D + k]);
+            acc = fmaf(__half2float(qr[k]), w, acc);
+        }
+        c2s[x] = __fmul_rn(acc, p.scale);
+    }
+}
+
+// PAIR_D > 0: the pair kernel's score-checksum layout (16 cols: c1_hi 0..7, c1_lo 8..15;
+// c2 recomputed by pair_score_c2)
+template <bool DBG, int PAIR_D = 0>
 __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr, uint32_t cs_addr,
                                             int head, int bi, int j, int row, bool exp_affected,
                                             float exp_first_residual, int exp_first_viol,
                                             float m_old, float& m_new, float& bm_hist,
                                             float* p_loc, int& replaced, ThreadTap& tap,
                                             int sc_fault_col, float sc_fault_val,
-                                            const RowScratch& rs) {
+                                            const RowScratch& rs, uint32_t bo = 0) {
     float sc[kBlock], raw[kBlock];
     float c1s[kStride], c2s[kStride];
     {
@@ -42,15 +62,25 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                 sc[c4 * 32 + x] = __fmul_rn(__uint_as_float(r[x]), p.scale);
             }
         }
-        uint32_t qh[16], ql[16];
-        tmem_ld16(cs_addr, qh);
-        tmem_ld16(cs_addr + 16, ql);
-        tmem_wait_ld();
+        if constexpr (PAIR_D > 0) {
+            uint32_t q[16];
+            tmem_ld16(cs_addr, q);
+            tmem_wait_ld();
 #pragma unroll
-        for (int x = 0; x < kStride; ++x) {
-            c1s[x] = __fmul_rn(__fadd_rn(__uint_as_float(qh[x]), __uint_as_float(ql[x])), p.scale);
-            c2s[x] = __fmul_rn(__fadd_rn(__uint_as_float(qh[kStride + x]), __uint_as_float(ql[kStride + x])),
-                               p.scale);
+            for (int x = 0; x < kStride; ++x)
+                c1s[x] = __fmul_rn(__fadd_rn(__uint_as_float(q[x]), __uint_as_float(q[kStride + x])), p.scale);
+            pair_score_c2<PAIR_D>(p, head, bi, j, row, c2s);
+        } else {
+            uint32_t qh[16], ql[16];
+            tmem_ld16(cs_addr, qh);
+            tmem_ld16(cs_addr + 16, ql);
+            tmem_wait_ld();
+#pragma unroll
+            for (int x = 0; x < kStride; ++x) {
+                c1s[x] = __fmul_rn(__fadd_rn(__uint_as_float(qh[x]), __uint_as_float(ql[x])), p.scale);
+                c2s[x] = __fmul_rn(__fadd_rn(__uint_as_float(qh[kStride + x]), __uint_as_float(ql[kStride + x])),
+                                   p.scale);
+            }
         }
     }
     if (DBG && sc_fault_col >= 0) sc[sc_fault_col] = sc_fault_val;  // GEMM1_OUT upset lives in sc
@@ -58,18 +88,18 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
     replaced = 0;
 
     // ---------------- exp stage (only if some row failed the product check)
-    const bool any_exp = named_bar_or(2, 128, exp_affected);
+    const bool any_exp = named_bar_or(2 + bo, 128, exp_affected);
     if (any_exp) {
         // (1) linear repair of the score tile (snvr.cpp:89-98)
         bool cs_bad = false;
 #pragma unroll
         for (int x = 0; x < kStride; ++x) cs_bad |= !isfinite(c1s[x]) || !isfinite(c2s[x]);
-        const bool tile_cs_bad = named_bar_or(2, 128, cs_bad);
+        const bool tile_cs_bad = named_bar_or(2 + bo, 128, cs_bad);
         RowVerify lin{};
         lin.best_col = -1;
         lin.restored_col = -1;
         if (!tile_cs_bad) verify_row<kBlock>(sc, c1s, c2s, p.eps_lin, lin);
-        TileReport lt = reduce_tile_report(lin, tile_cs_bad, row, rs.slots, rs.ints, rs.dbl);
+        TileReport lt = reduce_tile_report(lin, tile_cs_bad, row, rs.slots, rs.ints, rs.dbl, bo);
         // broadcast lin.row / corrections / status
         if (row == 0) {
             rs.ints[8] = lt.row;
@@ -82,7 +112,7 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
             rs.dbl[1] = lt.delta;
             rs.dbl[2] = 0.0;           // re-scan residual
         }
-        wg_sync();
+        wg_sync(bo);
         const int lin_row = rs.ints[9] > 0 ? rs.ints[8] : -1;
         const int lin_status = rs.ints[10];
         const bool affected = exp_affected || (row == lin_row);
@@ -146,10 +176,10 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                 atomicAdd(&rs.ints[14], 1);
             }
         }
-        const bool any_bad = named_bar_or(3, 128, still_bad);
+        const bool any_bad = named_bar_or(3 + bo, 128, still_bad);
         // tile residual / violations of the first look
         if (row == 0) { rs.ints[15] = 0; rs.dbl[3] = 0.0; }
-        wg_sync();
+        wg_sync(bo);
         atomicAdd(&rs.ints[15], exp_first_viol);
         {
             unsigned long long* a = reinterpret_cast<unsigned long long*>(&rs.dbl[3]);
@@ -161,7 +191,7 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                 old = atomicCAS(a, assumed, __double_as_longlong(v));
             } while (old != assumed);
         }
-        wg_sync();
+        wg_sync(bo);
         if (row == 0) {
             const int corrections = rs.ints[9] + rs.ints[14];
             int status;
@@ -175,7 +205,7 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
             push_event(p, EFTA_EXP_CHECKSUM, head, bi, j, status, erow, ecol, rs.ints[15], corrections,
                        0, rs.dbl[3], rs.ints[9] > 0 ? rs.dbl[1] : 0.0);
         }
-        wg_sync();
+        wg_sync(bo);
     }
 
     // ---------------- rescale-factor guard (efta.cpp:192-230), per row

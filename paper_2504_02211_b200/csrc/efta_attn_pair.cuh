@@ -1,21 +1,28 @@
 // efta_attn_pair.cuh — CTA-pair (cta_group::2) variant of the fused EFTA forward.
 //
-// Why: with one 128-row query tile per SM, every SM streams the full K_j / V_j tiles
-// of its head from L2 each iteration (64 KB, 88 KB protected, at d=128); the measured
-// iteration time sits at the chip's L2->SM delivery limit while the tensor cores idle
-// (tools/mma_bench.cu: every MMA flavour runs at its floor in isolation). A cluster of
-// two CTAs on one TPC computes an M=256 tile with tcgen05.mma.cta_group::2: each CTA
-// keeps its own 128 query rows (A) and holds only HALF of each B operand in its shared
-// memory, so per-SM ingress halves (32 KB / 40 KB per iteration).
+// Why a pair: with one 128-row query tile per SM, every SM streams the full K_j / V_j
+// tiles of its head from L2 each block. A cluster of two CTAs on one TPC computes an
+// M=256 tile with tcgen05.mma.cta_group::2: each CTA keeps its own 128 query rows (A)
+// and holds only HALF of each B operand in its shared memory, so per-SM ingress halves.
 //
 // B-operand split (CUTLASS 2x1SM traits: CTA v owns B rows [v*N/2, (v+1)*N/2)):
-//   S  = Q . [K_j ; KC_j]^T  N = 128 (+32):  leader K rows 0..63 (0..79),
-//                                            peer   K rows 64..127 (80..127 + KC 0..31)
+//   S  = Q . [K_j ; KC1_j]^T  N = 128 (+16): leader K rows 0..63 (0..71),
+//                                             peer   K rows 64..127 (72..127 + c1_hi, c1_lo)
+//        Only the c1 checksum rows (hi/lo) ride in the score MMA; c2, needed only to locate
+//        a fault once c1 flagged one, is recomputed on the CUDA cores in the rare path
+//        (pair_score_c2), so the checksum MMA work is +12.5% instead of +25%.
 //   O += P . [V_j | VC_j]    N = d (+32), B = [V_j^T ; VC_j^T] K-major (keys contiguous),
 //                            written by the encode prepass; each CTA loads (d+32)/2 rows.
+//
+// TMEM (512 columns): S[0] | S[1] (SW = 144 / 128 each) | O (d + 32 / d) | P (64, fp16x2).
+// P has its own buffer, so the score MMA of block j+2 can overwrite S[j&1] as soon as the
+// row warpgroup has read S_j (s_free), long before P.V of block j ran: the two row
+// warpgroups of the alternating schedule (efta_attn_alt.cuh) then never wait for scores.
+// The single P buffer is shared: block j's P is stored after P.V(j-1) completed.
+//
 // The leader (cluster rank 0) issues every MMA and multicasts its commits to both CTAs'
-// barriers; both CTAs' TMA loads signal the leader's full barriers; both row warpgroups
-// signal the leader's p_ready. The row warpgroup code is the single-CTA one (row_wg).
+// barriers; both CTAs' TMA loads signal the leader's full barriers; both CTAs' row
+// warpgroups signal the leader's s_free / p_ready barriers.
 #pragma once
 #include "efta_attn_kernel.cuh"
 
@@ -24,8 +31,9 @@ namespace efta_sm100 {
 template <int D, bool PROT>
 struct PairLayout {
     static constexpr int NSUB = D / 64;
-    static constexpr int HN_S = (PROT ? 160 : 128) / 2;  // B rows per CTA, scores
-    static constexpr int VROWS = PROT ? D + 32 : D;      // rows of the V^T (+VC^T) operand
+    static constexpr int SW = PROT ? 144 : 128;          // score MMA N (TMEM columns per S buffer)
+    static constexpr int HN_S = SW / 2;                  // B rows per CTA, scores
+    static constexpr int VROWS = PROT ? D + 32 : D;      // rows of the V^T (+VC^T) operand = O columns
     static constexpr int HN_V = VROWS / 2;               // B rows per CTA, P.V
     static constexpr int KS = 4, VS = 4;
     static constexpr uint32_t Q_BYTES = NSUB * 16384;
@@ -37,13 +45,22 @@ struct PairLayout {
     static constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
     static constexpr uint32_t OFF_V = OFF_K + KS * K_STAGE;
     static constexpr uint32_t OFF_BAR = OFF_V + VS * V_STAGE;
-    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2;
+    // q_full, k_full/empty[KS], v_full/empty[VS], s_full[2], s_free[2], p_ready[2],
+    // o_done[2], o_final, chain barriers mx_early[2][4], mx_late[2][4]
+    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2 + 2 + 2 + 1 + 16;
     static constexpr uint32_t OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
-    static constexpr uint32_t RED_BYTES = 128 * 24 + 256;
-    static constexpr uint32_t SMEM_BYTES = OFF_RED + RED_BYTES + 1024;
+    static constexpr uint32_t RED_BYTES = 128 * 24 + 256;  // per row warpgroup
+    static constexpr uint32_t OFF_XCH = OFF_RED + 2 * RED_BYTES;
+    static constexpr uint32_t SMEM_BYTES = OFF_XCH + 6144 + 1024;
+    // TMEM columns
+    static constexpr uint32_t COL_S0 = 0, COL_O = 2 * SW, COL_P = COL_O + VROWS, TMEM_COLS = 512;
+    static_assert(COL_P + 64 <= TMEM_COLS, "TMEM budget");
     static_assert(K_CHUNK % 1024 == 0 && V_CHUNK % 1024 == 0, "swizzle atoms must stay 1 KB aligned");
+    static_assert(RED_BYTES == AttnLayout<D>::RED_BYTES, "row scratch size");
+    static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
+constexpr int kPairThreads = 384;  // warps 0-3: TMA K / score MMA / P.V MMA / TMA Q,V; 4-7, 8-11: row warpgroups
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -94,16 +111,21 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* tma
         : "memory");
 }
 
-// tm_ka: K rows [0, HN_S) (or [64r, 64r+64) unprotected), tm_kb: K rows 80..127 (protected),
-// tm_kc: KC (protected), tm_vt: [V^T ; VC^T] rows of each block, box rows HN_V.
+}  // namespace efta_sm100
+
+#include "efta_attn_alt.cuh"
+
+namespace efta_sm100 {
+
+// tm_ka: K rows [0, HN_S) (or [64r, 64r+64) unprotected), tm_kb: K rows 72..127 (protected),
+// tm_kc: KC rows in 8-row boxes (protected), tm_vt: [V^T ; VC^T] rows of each block, box rows HN_V.
 template <int D, int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_ka,
                       const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_kc,
                       const __grid_constant__ CUtensorMap tm_vt, const AttnParams p) {
     constexpr bool PROT = MODE != EFTA_MODE_NONE;
     using L = PairLayout<D, PROT>;
-    using TL = AttnLayout<D>;  // TMEM column plan (shared with the single-CTA kernel)
     constexpr int KS = L::KS, VS = L::VS, NSUB = L::NSUB;
 
     extern __shared__ uint8_t smem_raw[];
@@ -114,9 +136,13 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     uint64_t* k_empty = k_full + KS;
     uint64_t* v_full = k_empty + KS;
     uint64_t* v_empty = v_full + VS;
-    uint64_t* s_full = v_empty + VS;
-    uint64_t* p_ready = s_full + 2;
-    uint64_t* o_done = p_ready + 1;
+    uint64_t* s_full = v_empty + VS;   // [2] by block parity
+    uint64_t* s_free = s_full + 2;     // [2] row warpgroup w has read S_j (leader)
+    uint64_t* p_ready = s_free + 2;    // [2] P_j stored / O rescaled (leader)
+    uint64_t* o_done = p_ready + 2;    // [2] P.V of block j complete
+    uint64_t* o_final = o_done + 2;
+    uint64_t* mx_early = o_final + 1;  // [2][4]
+    uint64_t* mx_late = mx_early + 8;  // [2][4]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
     const int warp = warp_id(), lane = lane_id();
@@ -128,17 +154,21 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         mbar_init(q_full, 1);
         for (int s = 0; s < KS; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
         for (int s = 0; s < VS; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
-        mbar_init(&s_full[0], 1);
-        mbar_init(&s_full[1], 1);
-        mbar_init(p_ready, 8);  // 4 row warps x 2 CTAs
-        mbar_init(o_done, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&s_full[b], 1);
+            mbar_init(&s_free[b], 8);   // 4 row warps x 2 CTAs
+            mbar_init(&p_ready[b], 8);
+            mbar_init(&o_done[b], 1);
+        }
+        mbar_init(o_final, 1);
+        for (int i = 0; i < 16; ++i) mbar_init(&mx_early[i], 32);
         fence_barrier_init();
         tma_prefetch_desc(&tm_q);
         tma_prefetch_desc(&tm_ka);
         tma_prefetch_desc(&tm_vt);
         if (PROT) { tma_prefetch_desc(&tm_kb); tma_prefetch_desc(&tm_kc); }
     }
-    if (warp == 1) tmem_alloc2(tmem_slot, TL::TMEM_COLS);
+    if (warp == 1) tmem_alloc2(tmem_slot, L::TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
@@ -149,7 +179,8 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     const uint32_t v_smem = smem_u32(smem + L::OFF_V);
 
     if (warp == 0) {
-        // -------------------------------------------------------- K (+KC) half producer
+        // -------------------------------------------------------- K (+KC1) half producer
+        setmaxnreg_dec<40>();
         if (lane == 0) {
             for (int j = 0; j < n; ++j) {
                 const int s = j % KS;
@@ -157,6 +188,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                 uint8_t* dst = smem + L::OFF_K + s * L::K_STAGE;
                 if (rank == 0) mbar_arrive_expect_tx(&k_full[s], 2 * L::K_STAGE);
                 const int krow = seq_row0 + j * kBlock;
+                const int crow = (head * n + j) * 32;
 #pragma unroll
                 for (int sub = 0; sub < NSUB; ++sub) {
                     uint8_t* c = dst + sub * L::K_CHUNK;
@@ -165,15 +197,16 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                     } else if (rank == 0) {
                         tma_load_2d_pair(c, &tm_ka, &k_full[s], sub * 64, krow, kEvictLast);
                     } else {
-                        tma_load_2d_pair(c, &tm_kb, &k_full[s], sub * 64, krow + 80, kEvictLast);
-                        tma_load_2d_pair(c + 48 * 128, &tm_kc, &k_full[s], sub * 64, (head * n + j) * 32,
-                                         kEvictLast);
+                        tma_load_2d_pair(c, &tm_kb, &k_full[s], sub * 64, krow + 72, kEvictLast);
+                        tma_load_2d_pair(c + 56 * 128, &tm_kc, &k_full[s], sub * 64, crow, kEvictLast);       // c1_hi
+                        tma_load_2d_pair(c + 64 * 128, &tm_kc, &k_full[s], sub * 64, crow + 16, kEvictLast);  // c1_lo
                     }
                 }
             }
         }
     } else if (warp == 3) {
         // -------------------------------------------------------- Q, V^T (+VC^T) half producer
+        setmaxnreg_dec<40>();
         if (lane == 0) {
             if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * L::Q_BYTES);
 #pragma unroll
@@ -192,64 +225,85 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             }
         }
     } else if (warp == 1) {
-        // -------------------------------------------------------- MMA issuer (pair leader only)
-        if (lane == 0 && rank == 0) {
-            constexpr uint32_t ID_S = idesc_f16_f32(256, PROT ? 160 : 128, 0, 0);
-            constexpr uint32_t ID_PV = idesc_f16_f32(256, L::VROWS, 0, 0);
+        // -------------------------------------------------------- score MMA issuer (pair leader)
+        // S_j = Q . [K_j ; KC1_j]^T into S[j&1]; S_{j+2} once both CTAs' warpgroup read S_j.
+        // Two issuer threads: a single one idles the tensor pipe while it waits on the
+        // other operand's barriers (the tcgen05 queue is shallow, tools/mma2_bench.cu).
+        setmaxnreg_dec<40>();
+        if (rank == 0) {  // the whole warp runs the loop; one elected lane issues
+            constexpr uint32_t ID_S = idesc_f16_f32(256, L::SW, 0, 0);
+            const uint64_t dq = smem_desc_sw128(q_smem, 16, 1024);
+            const uint64_t dk0 = smem_desc_sw128(k_smem, 16, 1024);
             mbar_wait(q_full, 0);
             tc_fence_after();
-            auto issue_s = [&](int j) {
+            for (int j = 0; j < n; ++j) {
+                if (j >= 2) {
+                    mbar_wait(&s_free[j & 1], ((j - 2) >> 1) & 1);
+                    EFTA_TS(7, j - 2);
+                }
                 const int s = j % KS;
                 mbar_wait(&k_full[s], (j / KS) & 1);
+                EFTA_TS(8, j - 2);
                 tc_fence_after();
-                const uint32_t kb = k_smem + s * L::K_STAGE;
-                const uint32_t d_s = tmem + TL::COL_S0 + (j & 1) * TL::S_STRIDE;
+                const uint64_t dk = dk0 + ((s * L::K_STAGE) >> 4);
+                const uint32_t d_s = tmem + L::COL_S0 + (j & 1) * L::SW;
+                if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t offq = (kk >> 2) * 16384 + (kk & 3) * 32;
-                    const uint32_t offk = (kk >> 2) * L::K_CHUNK + (kk & 3) * 32;
-                    mma2_ss(d_s, smem_desc_sw128(q_smem + offq, 16, 1024), smem_desc_sw128(kb + offk, 16, 1024),
-                            ID_S, kk > 0);
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t offq = (kk >> 2) * 16384 + (kk & 3) * 32;
+                        const uint32_t offk = (kk >> 2) * L::K_CHUNK + (kk & 3) * 32;
+                        mma2_ss(d_s, dq + (offq >> 4), dk + (offk >> 4), ID_S, kk > 0);
+                    }
+                    commit2_both(&k_empty[s]);
+                    commit2_both(&s_full[j & 1]);
                 }
-                commit2_both(&k_empty[s]);
-                commit2_both(&s_full[j & 1]);
-            };
-            issue_s(0);
+                __syncwarp();
+                EFTA_TS(11, j - 2);
+            }
+        }
+    } else if (warp == 2) {
+        // -------------------------------------------------------- P.V MMA issuer (pair leader)
+        setmaxnreg_dec<40>();
+        if (rank == 0) {
+            constexpr uint32_t ID_PV = idesc_f16_f32(256, L::VROWS, 0, 0);
+            const uint64_t dv0 = smem_desc_sw128(v_smem, 16, 1024);
+            const uint32_t a_p = tmem + L::COL_P, d_o = tmem + L::COL_O;
             for (int j = 0; j < n; ++j) {
                 EFTA_TS(10, j);
-                if (j + 1 < n) issue_s(j + 1);
-                EFTA_TS(11, j);
-                mbar_wait(p_ready, j & 1);
+                mbar_wait(&p_ready[j & 1], (j >> 1) & 1);
                 EFTA_TS(12, j);
                 tc_fence_after();
                 const int s = j % VS;
                 mbar_wait(&v_full[s], (j / VS) & 1);
                 EFTA_TS(14, j);
                 tc_fence_after();
-                const uint32_t vb = v_smem + s * L::V_STAGE;
-                const uint32_t a_p = tmem + TL::COL_S0 + (j & 1) * TL::S_STRIDE;
+                const uint64_t dv = dv0 + ((s * L::V_STAGE) >> 4);
+                if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < kBlock / 16; ++kk) {
-                    const uint32_t offv = (kk >> 2) * L::V_CHUNK + (kk & 3) * 32;
-                    mma2_ts(tmem + TL::COL_O, a_p + kk * 8, smem_desc_sw128(vb + offv, 16, 1024), ID_PV,
-                            (j > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < kBlock / 16; ++kk) {
+                        const uint32_t offv = (kk >> 2) * L::V_CHUNK + (kk & 3) * 32;
+                        mma2_ts(d_o, a_p + kk * 8, dv + (offv >> 4), ID_PV, (j > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    commit2_both(&v_empty[s]);
+                    commit2_both(&o_done[j & 1]);
+                    if (j == n - 1) commit2_both(o_final);
                 }
-                commit2_both(&v_empty[s]);
-                commit2_both(o_done);
+                __syncwarp();
                 EFTA_TS(13, j);
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
-        row_wg<D, MODE, false, true>(p, smem + L::OFF_RED, s_full, p_ready, o_done, tmem, warp, lane, head, qt,
-                                     n, seq_row0);
+    } else {
+        setmaxnreg_inc<232>();
+        row_alt<D, PROT>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH), s_full, s_free,
+                         p_ready, o_done, o_final, mx_early, mx_late, tmem, warp, lane, head, qt, n, seq_row0);
     }
 
     tc_fence_before();
     __syncthreads();
     cluster_sync_all();  // the peer may still be reading our shared memory / TMEM via the MMAs
     tc_fence_after();
-    if (warp == 1) tmem_dealloc2(tmem, TL::TMEM_COLS);
+    if (warp == 1) tmem_dealloc2(tmem, L::TMEM_COLS);
 }
 
 // Prepass for the pair kernel: KC (as before) + [V_j^T ; VC_j^T] per (head, block):

@@ -199,11 +199,13 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
             if (e != cudaSuccess) return fail(2, std::string("encode: ") + cudaGetErrorString(e));
         }
         const int vrows = prot ? D + 32 : D;
-        ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, rows, D, prot ? 80 : 64) &&
+        // score operand N = 144 (protected: K + c1_hi + c1_lo rows) or 128, half per CTA:
+        // leader K rows 0..71 (0..63), peer K rows 72..127 + two 8-row KC boxes (64..127)
+        ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, rows, D, prot ? 72 : 64) &&
              make_map(&tvc, r2, static_cast<uint64_t>(bh) * nblk * vrows, 128, vrows / 2);
         if (prot)
-            ok = ok && make_map(&tv, k, rows, D, 48) &&
-                 make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 32);
+            ok = ok && make_map(&tv, k, rows, D, 56) &&
+                 make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 8);
         else {
             tv = tk;
             tkc = tk;
@@ -257,6 +259,8 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     p.exp_lo = std::isfinite(d->eps1) ? static_cast<float>(std::exp(-d->eps1)) : 0.0f;
     p.exp_hi = std::isfinite(d->eps1) ? static_cast<float>(std::exp(d->eps1)) : INFINITY;
     p.scratch = wsb ? reinterpret_cast<float*>(wsb + wl.scratch) : nullptr;
+    p.q = reinterpret_cast<const __half*>(q);
+    p.kc = reinterpret_cast<const __half*>(kc);
     const bool dbg = d->debug != 0;
     cudaError_t e;
     if (pair)  // maps: q, K half A, K half B (protected peer), KC, [V^T ; VC^T]
