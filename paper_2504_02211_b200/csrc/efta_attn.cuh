@@ -67,15 +67,23 @@ struct AttnParams {
 };
 
 #ifdef EFTA_PROF
-// phase timestamps (clock64) of CTAs (2,5) and (3,5): row warp 4 lane 0 and the MMA thread
+// phase timestamps (clock64) of CTA (2,5) (a pair leader): lane 0 of the stamping warp;
+// EFTA_TSQ stamps all four warps of a row warpgroup at slots 16 + base + warp quarter
 #define EFTA_TS(slot, j)                                                                       \
     do {                                                                                       \
-        if (p.prof && (blockIdx.x == 2 || blockIdx.x == 3) && blockIdx.y == 5 &&                 \
-            (threadIdx.x & 31) == 0 && (j) >= 0 && (j) < 64)                                               \
-            p.prof[(j) * 32 + (blockIdx.x & 1) * 16 + (slot)] = clock64();                       \
+        if (p.prof && blockIdx.x == 2 && blockIdx.y == 5 &&                                    \
+            (threadIdx.x & 31) == 0 && (j) >= 0 && (j) < 64)                                   \
+            p.prof[(j) * 32 + (slot)] = clock64();                                             \
+    } while (0)
+#define EFTA_TSQ(base, j)                                                                      \
+    do {                                                                                       \
+        if (p.prof && blockIdx.x == 2 && blockIdx.y == 5 &&                                    \
+            (threadIdx.x & 31) == 0 && (j) >= 0 && (j) < 64)                                   \
+            p.prof[(j) * 32 + 16 + (base) + ((threadIdx.x >> 5) & 3)] = clock64();              \
     } while (0)
 #else
 #define EFTA_TS(slot, j) do { } while (0)
+#define EFTA_TSQ(base, j) do { } while (0)
 #endif
 
 constexpr int kScratchSMs = 256;

@@ -82,6 +82,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         if ((warp & 3) == 0) EFTA_TS(0, j);
         mbar_wait(&s_full[w], it & 1);
         if ((warp & 3) == 0) EFTA_TS(1, j);
+        EFTA_TSQ(8, j);
         tc_fence_after();
         const uint32_t pph = static_cast<uint32_t>((j - 1) >> 1) & 1u;  // partner's phase for block j-1
         float pv[kBlock];
@@ -128,6 +129,8 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                 xc->early[w][row] = make_float2(m_true, m_new);
                 mbar_arrive(my_early);
             }
+            if ((warp & 3) == 0) EFTA_TS(15, j);
+            EFTA_TSQ(4, j);
             const float mL = m_new * kLog2e;
             float pc1v[kStride];
             float2 prod_f[kStride / 2];
@@ -153,10 +156,14 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                 pv[c + 1] = e.y;
                 if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
                 else ps0 = fadd2(ps0, e);
+#ifndef EFTA_ABL_NOPROD
                 if (PROT) {
                     const int g = (c & 7) >> 1;
                     prod_f[g] = (c < kStride) ? e : fmul2(prod_f[g], e);
                 }
+#else
+                if (PROT && c < kStride) prod_f[(c & 7) >> 1] = e;
+#endif
             }
             psum_f = (ps0.x + ps0.y) + (ps1.x + ps1.y);
             if (!PROT) break;  // no recovery path: the chain can never be revised
@@ -173,18 +180,30 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                 if (bad) { exp_affected = true; ++exp_viol; }
             }
             float exp_res = 0.0f;
+#ifdef EFTA_ABL_NOPROD  // timing ablation only: no exp-stage check
+            exp_affected = false;
+            exp_viol = 0;
+#endif
             if (degenerate) { exp_affected = true; exp_res = CUDART_INF_F; exp_viol = 1; }
             const bool factor_bad = (j > 0) && !(f > 0.0f && f <= 1.0f);
             // ---- late chain check: did the partner's decision revise block j-1's maxima?
             bool chain_bad = false;
             if (j > 0) {
+                if ((warp & 3) == 0) EFTA_TS(8, j);
+#ifndef EFTA_ABL_NOLATE
                 if (attempt == 0) mbar_wait(pa_late, pph);
+#endif
                 const float2 c = xc->late[1 - w][row];
                 chain_bad = __float_as_uint(c.x) != __float_as_uint(m_true_prev) ||
                             __float_as_uint(c.y) != __float_as_uint(m_run_prev);
             }
             if ((warp & 3) == 0) EFTA_TS(9, j);
+            EFTA_TSQ(0, j);
+#ifdef EFTA_ABL_NOBAR  // timing ablation only: no tile-wide decision
+            if (!__any_sync(0xffffffffu, exp_affected || factor_bad || chain_bad)) break;
+#else
             if (!named_bar_or(6 + bo, 128, exp_affected || factor_bad || chain_bad)) break;
+#endif
             if (named_bar_or(6 + bo, 128, chain_bad)) continue;  // redo the block with the revised maxima
             // ---- rare: the reference recovery ladder for this tile
             float p_loc[kBlock];
@@ -227,25 +246,26 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         l_w = __fadd_rn(__fmul_rn(fw, l_w), psum);
 
         if ((warp & 3) == 0) EFTA_TS(3, j);
-        // ---- P (fp16) into the shared P buffer, once P.V of block j-1 has consumed it
-        if (j > 0) {
+        // ---- P (fp16): packed first, stored once the P buffer is free (P.V of block j-1
+        // with one shared buffer, of block j-2 with one buffer per warpgroup)
+        uint32_t pk[64];
+#pragma unroll
+        for (int x = 0; x < 64; ++x) pk[x] = pack_half2(pv[2 * x], pv[2 * x + 1]);
+        const bool need_o = j > 0 && !__all_sync(0xffffffffu, fo == 1.0f);
+        if (L::NPB == 1 ? (j > 0) : (j >= 2 || need_o)) {
             if ((warp & 3) == 0) EFTA_TS(4, j);
-            mbar_wait(&o_done[1 - w], static_cast<uint32_t>((j - 1) >> 1) & 1u);
+            if (L::NPB == 1 || need_o)
+                mbar_wait(&o_done[1 - w], static_cast<uint32_t>((j - 1) >> 1) & 1u);
+            else
+                mbar_wait(&o_done[w], static_cast<uint32_t>((j - 2) >> 1) & 1u);
             if ((warp & 3) == 0) EFTA_TS(5, j);
             tc_fence_after();
         }
-        {
-            uint32_t pk[32];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                for (int x = 0; x < 32; ++x) pk[x] = pack_half2(pv[h * 64 + 2 * x], pv[h * 64 + 2 * x + 1]);
-                tmem_st32(lane_base + L::COL_P + h * 32, pk);
-            }
-        }
+        tmem_st32(lane_base + L::COL_P + w * (L::NPB - 1) * 64, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        tmem_st32(lane_base + L::COL_P + w * (L::NPB - 1) * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
         // ---- O *= fo (lazy: only when this block moved the reference max of some row);
         // P.V of block j-1 is complete (waited above)
-        if (j > 0 && !__all_sync(0xffffffffu, fo == 1.0f)) {
+        if (need_o) {
             constexpr int NCH = D / 32 + (PROT ? 1 : 0);
             float o[NCH][32];
 #pragma unroll
@@ -269,6 +289,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         tc_fence_before();
         signal_p_ready<true>(&p_ready[w], lane);
         if ((warp & 3) == 0) EFTA_TS(6, j);
+        EFTA_TSQ(12, j);
         m_ref = m_new;
         m_true_last = m_true;
     }

@@ -18,7 +18,8 @@
 // P has its own buffer, so the score MMA of block j+2 can overwrite S[j&1] as soon as the
 // row warpgroup has read S_j (s_free), long before P.V of block j ran: the two row
 // warpgroups of the alternating schedule (efta_attn_alt.cuh) then never wait for scores.
-// The single P buffer is shared: block j's P is stored after P.V(j-1) completed.
+// With one P buffer per warpgroup (when TMEM allows) block j's P only waits for P.V(j-2);
+// the protected d=128 layout shares one buffer: block j's P is stored after P.V(j-1).
 //
 // The leader (cluster rank 0) issues every MMA and multicasts its commits to both CTAs'
 // barriers; both CTAs' TMA loads signal the leader's full barriers; both CTAs' row
@@ -55,7 +56,10 @@ struct PairLayout {
     static constexpr uint32_t SMEM_BYTES = OFF_XCH + 6144 + 1024;
     // TMEM columns
     static constexpr uint32_t COL_S0 = 0, COL_O = 2 * SW, COL_P = COL_O + VROWS, TMEM_COLS = 512;
-    static_assert(COL_P + 64 <= TMEM_COLS, "TMEM budget");
+    // one P buffer per row warpgroup when it fits (unprotected d=128, every d=64 variant);
+    // protected d=128 (2*144 + 160 + 64 = 512) shares one
+    static constexpr int NPB = (COL_P + 128 <= TMEM_COLS) ? 2 : 1;
+    static_assert(COL_P + 64 * NPB <= TMEM_COLS, "TMEM budget");
     static_assert(K_CHUNK % 1024 == 0 && V_CHUNK % 1024 == 0, "swizzle atoms must stay 1 KB aligned");
     static_assert(RED_BYTES == AttnLayout<D>::RED_BYTES, "row scratch size");
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
@@ -243,7 +247,6 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                 }
                 const int s = j % KS;
                 mbar_wait(&k_full[s], (j / KS) & 1);
-                EFTA_TS(8, j - 2);
                 tc_fence_after();
                 const uint64_t dk = dk0 + ((s * L::K_STAGE) >> 4);
                 const uint32_t d_s = tmem + L::COL_S0 + (j & 1) * L::SW;
@@ -267,7 +270,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         if (rank == 0) {
             constexpr uint32_t ID_PV = idesc_f16_f32(256, L::VROWS, 0, 0);
             const uint64_t dv0 = smem_desc_sw128(v_smem, 16, 1024);
-            const uint32_t a_p = tmem + L::COL_P, d_o = tmem + L::COL_O;
+            const uint32_t d_o = tmem + L::COL_O;
             for (int j = 0; j < n; ++j) {
                 EFTA_TS(10, j);
                 mbar_wait(&p_ready[j & 1], (j >> 1) & 1);
@@ -278,6 +281,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                 EFTA_TS(14, j);
                 tc_fence_after();
                 const uint64_t dv = dv0 + ((s * L::V_STAGE) >> 4);
+                const uint32_t a_p = tmem + L::COL_P + (L::NPB == 2 ? (j & 1) * 64 : 0);
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < kBlock / 16; ++kk) {

@@ -29,7 +29,7 @@ cudart = C.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libc
 cudart.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
 cudart.cudaMemcpy(buf.ctypes.data, ptr, buf.nbytes, 2)
 t = buf.reshape(64, 32).astype(np.int64)
-names = {7: "mma:s_free", 8: "mma:k_full+2", 0: "row:wait_S", 1: "row:S_ready", 2: "row:exp_done", 3: "row:sum_done", 4: "row:P_stored",
+names = {7: "mma:s_free", 8: "row:pre_late", 15: "row:pre_exp", 0: "row:wait_S", 1: "row:S_ready", 2: "row:exp_done", 3: "row:sum_done", 4: "row:P_stored",
          5: "row:O_ready", 6: "row:p_ready", 10: "mma:iter", 11: "mma:S_issued", 12: "mma:P_ready",
          14: "mma:V_ready", 13: "mma:PV_issued", 16: "peer:wait_S", 17: "peer:S_ready", 18: "peer:exp_done",
          22: "peer:p_ready"}
