@@ -146,7 +146,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             for (int c = 0; c < kBlock; c += 2) {
                 const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
                 float2 e;
-                if (exp_on_fma(c)) {
+                if (exp_on_fma<D>(c)) {
                     e = ex2_poly2(a);
                 } else {
                     e.x = ex2_approx(a.x);
@@ -210,7 +210,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
 #pragma unroll
             for (int c = 0; c < kBlock; ++c) p_loc[c] = pv[c];
             int replaced = 0;
-            exp_stage_slow<false, D>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res, exp_viol,
+            exp_stage_slow<false, D, true>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res, exp_viol,
                                   m_run_prev, m_new, bm, p_loc, replaced, tap, -1, 0.0f, rs, bo);
             if (replaced) {
 #pragma unroll

@@ -38,9 +38,9 @@ __device__ __noinline__ void pair_score_c2(const AttnParams& p, int head, int bi
     }
 }
 
-// PAIR_D > 0: the pair kernel's score-checksum layout (16 cols: c1_hi 0..7, c1_lo 8..15;
+// PAIR: the pair kernel's score-checksum layout (16 cols: c1_hi 0..7, c1_lo 8..15;
 // c2 recomputed by pair_score_c2)
-template <bool DBG, int PAIR_D = 0>
+template <bool DBG, int D, bool PAIR>
 __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr, uint32_t cs_addr,
                                             int head, int bi, int j, int row, bool exp_affected,
                                             float exp_first_residual, int exp_first_viol,
@@ -62,14 +62,14 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                 sc[c4 * 32 + x] = __fmul_rn(__uint_as_float(r[x]), p.scale);
             }
         }
-        if constexpr (PAIR_D > 0) {
+        if constexpr (PAIR) {
             uint32_t q[16];
             tmem_ld16(cs_addr, q);
             tmem_wait_ld();
 #pragma unroll
             for (int x = 0; x < kStride; ++x)
                 c1s[x] = __fmul_rn(__fadd_rn(__uint_as_float(q[x]), __uint_as_float(q[kStride + x])), p.scale);
-            pair_score_c2<PAIR_D>(p, head, bi, j, row, c2s);
+            pair_score_c2<D>(p, head, bi, j, row, c2s);
         } else {
             uint32_t qh[16], ql[16];
             tmem_ld16(cs_addr, qh);
@@ -141,7 +141,7 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                     // same formula as the fast path so untouched cells reproduce their bits;
                     // a linearly repaired cell only exists in the scaled domain
                     e = (__fmul_rn(raw[c], p.scale) == sc[c])
-                            ? ex2_col(c, fmaf(raw[c], scale_log2, -mL))
+                            ? ex2_col<D>(c, fmaf(raw[c], scale_log2, -mL))
                             : ex2_approx(__fsub_rn(sc[c], mm) * kLog2e);
                 }
                 if (__float_as_uint(e) != __float_as_uint(p_loc[c])) changed = 1;
@@ -230,7 +230,7 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                     e = tap(p, EFTA_EXP_OUT, j, c, e);
                 } else {
                     e = (__fmul_rn(raw[c], p.scale) == sc[c])
-                            ? ex2_col(c, fmaf(raw[c], scale_log2, -mL))
+                            ? ex2_col<D>(c, fmaf(raw[c], scale_log2, -mL))
                             : ex2_approx(__fsub_rn(sc[c], mm) * kLog2e);
                 }
                 p_loc[c] = e;
@@ -476,7 +476,7 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
             for (int c = 0; c < kBlock; c += 2) {
                 const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
                 float2 e;
-                if (exp_on_fma(c)) {
+                if (exp_on_fma<D>(c)) {
                     e = ex2_poly2(a);
                 } else {
                     e.x = ex2_approx(a.x);
@@ -549,7 +549,7 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
                 for (int c = 0; c < kBlock; ++c) p_loc[c] = pv[c];
                 int replaced = 0;
                 const float m_true_prev = m_true_before;
-                exp_stage_slow<DBG>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res,
+                exp_stage_slow<DBG, D, false>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res,
                                     exp_viol, m_run, m_new, bm, p_loc, replaced, tap, sc_fault_col,
                                     sc_fault_val, rs);
                 if (replaced) {

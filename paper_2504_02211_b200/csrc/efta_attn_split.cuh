@@ -136,7 +136,7 @@ __device__ __forceinline__ void row_split(const AttnParams& p, uint64_t* s_full,
                 if (half == 0) {
                     float p_loc[kBlock];
                     for (int c = 0; c < 64; ++c) { p_loc[c] = pv[c]; p_loc[64 + c] = scr[64 + c]; }
-                    exp_stage_slow<false>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res,
+                    exp_stage_slow<false, D, false>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res,
                                           exp_viol, m_run, m_new, bm, p_loc, replaced, no_tap, -1,
                                           0.0f, rs);
                     if (replaced) {
