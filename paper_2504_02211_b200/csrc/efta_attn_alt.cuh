@@ -51,7 +51,8 @@ template <int D, bool PROT>
 __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, uint64_t* s_full,
                                         uint64_t* s_free, uint64_t* p_ready, uint64_t* o_done, uint64_t* o_final,
                                         uint64_t* mx_early, uint64_t* mx_late, uint32_t tmem, int warp,
-                                        int lane, int head, int qt, int n, int seq_row0) {
+                                        int lane, int head, int qt, int n, int seq_row0, const CUtensorMap* tm_o,
+                                        uint8_t* ostage) {
     using L = PairLayout<D, PROT>;
     constexpr int MODE = PROT ? EFTA_MODE_EFTA_OPT : EFTA_MODE_NONE;
     const int w = (warp - 4) >> 2;
@@ -380,20 +381,39 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             wg_sync();
         }
     }
-    // normalization (efta.cpp:312-327)
+    // normalization (efta.cpp:312-327): one IEEE reciprocal, then products (within 1 ulp of
+    // the reference's division; the tap kernel keeps the exact division)
+    const float rl = __frcp_rn(l_run);
 #pragma unroll
-    for (int c = 0; c < D; ++c) o[c] = __fdiv_rn(o[c], l_run);
+    for (int c = 0; c < D; c += 2) {
+        const float2 r2 = fmul2(make_float2(o[c], o[c + 1]), make_float2(rl, rl));
+        o[c] = r2.x;
+        o[c + 1] = r2.y;
+    }
     if (PROT) {
 #pragma unroll
-        for (int x = 0; x < kStride; ++x) { c1[x] = __fdiv_rn(c1[x], l_run); c2[x] = __fdiv_rn(c2[x], l_run); }
+        for (int x = 0; x < kStride; ++x) { c1[x] = __fmul_rn(c1[x], rl); c2[x] = __fmul_rn(c2[x], rl); }
         float res;
         verify_output_tile<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res);
         if (isfinite(res)) fam_out = fmaxf(fam_out, res);
     }
-    const size_t grow = static_cast<size_t>(seq_row0) + qt * kBlock + row;
-    float4* dst = reinterpret_cast<float4*>(p.o + grow * D);
+    // store: the O tile is staged in the (now idle) K ring in the 128B-swizzled layout of the
+    // fp32 O map (D/32 boxes of 32 columns x 128 rows) and written with TMA bulk stores
+    // (one thread-owned 512-byte row per lane would otherwise be 32 strided 16-byte stores)
 #pragma unroll
-    for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+    for (int c = 0; c < D / 4; ++c) {
+        const int cb = c >> 3, k = c & 7;
+        *reinterpret_cast<float4*>(ostage + cb * 16384 + row * 128 + ((k ^ (row & 7)) << 4)) =
+            make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+    }
+    fence_proxy_async_smem();
+    wg_sync();
+    if (row == 0) {
+#pragma unroll
+        for (int cb = 0; cb < D / 32; ++cb) tma_store_2d(tm_o, ostage + cb * 16384, cb * 32, seq_row0 + qt * kBlock);
+        bulk_commit_group();
+    }
+    const size_t grow = static_cast<size_t>(seq_row0) + qt * kBlock + row;
     if (p.m_out) p.m_out[grow] = m_run;
     if (p.l_out) p.l_out[grow] = l_run;
     if (PROT) {
@@ -401,6 +421,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         for (int off = 16; off > 0; off >>= 1) fam_out = fmaxf(fam_out, __shfl_xor_sync(0xffffffffu, fam_out, off));
         if (lane == 0) atomic_max_nonneg(&p.counters->family_max[1], fam_out);
     }
+    if (row == 0) bulk_wait_group_read0();  // shared memory stays valid until the stores read it
     (void)MODE;
 }
 

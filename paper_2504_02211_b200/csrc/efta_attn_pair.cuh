@@ -63,6 +63,7 @@ struct PairLayout {
     static_assert(K_CHUNK % 1024 == 0 && V_CHUNK % 1024 == 0, "swizzle atoms must stay 1 KB aligned");
     static_assert(RED_BYTES == AttnLayout<D>::RED_BYTES, "row scratch size");
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+    static_assert(KS * K_STAGE >= D * 128 * 4, "the epilogue stages the fp32 O tile in the idle K ring");
 };
 constexpr int kPairThreads = 384;  // warps 0-3: TMA K / score MMA / P.V MMA / TMA Q,V; 4-7, 8-11: row warpgroups
 
@@ -127,7 +128,8 @@ template <int D, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_ka,
                       const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_kc,
-                      const __grid_constant__ CUtensorMap tm_vt, const AttnParams p) {
+                      const __grid_constant__ CUtensorMap tm_vt, const __grid_constant__ CUtensorMap tm_o,
+                      const AttnParams p) {
     constexpr bool PROT = MODE != EFTA_MODE_NONE;
     using L = PairLayout<D, PROT>;
     constexpr int KS = L::KS, VS = L::VS, NSUB = L::NSUB;
@@ -300,7 +302,8 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     } else {
         setmaxnreg_inc<232>();
         row_alt<D, PROT>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH), s_full, s_free,
-                         p_ready, o_done, o_final, mx_early, mx_late, tmem, warp, lane, head, qt, n, seq_row0);
+                         p_ready, o_done, o_final, mx_early, mx_late, tmem, warp, lane, head, qt, n, seq_row0,
+                         &tm_o, smem + L::OFF_K);
     }
 
     tc_fence_before();
