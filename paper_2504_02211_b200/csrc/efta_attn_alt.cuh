@@ -50,9 +50,9 @@ static_assert(sizeof(AltXch) == 6144, "PairLayout reserves 6 KB for the chain ex
 template <int D, bool PROT>
 __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, uint64_t* s_full,
                                         uint64_t* s_free, uint64_t* p_ready, uint64_t* o_done, uint64_t* o_final,
-                                        uint64_t* mx_early, uint64_t* mx_late, uint32_t tmem, int warp,
-                                        int lane, int head, int qt, int n, int seq_row0, const CUtensorMap* tm_o,
-                                        uint8_t* ostage) {
+                                        uint64_t* mx_early, uint64_t* mx_late, uint64_t* fin_bar,
+                                        uint64_t* o_free, uint32_t tmem, int warp, int lane, int n, int cid,
+                                        int ncl, uint32_t rank) {
     using L = PairLayout<D, PROT>;
     constexpr int MODE = PROT ? EFTA_MODE_EFTA_OPT : EFTA_MODE_NONE;
     const int w = (warp - 4) >> 2;
@@ -73,19 +73,27 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     uint64_t* pa_early = mx_early + (1 - w) * 4 + wq;
     uint64_t* pa_late = mx_late + (1 - w) * 4 + wq;
     const float scale = p.scale, scale_log2 = p.scale_log2;
-    // own sums, referenced to m_ref (the reference max of this warpgroup's last block)
-    float l_w = 0.0f, lb_w = 0.0f, m_ref = -CUDART_INF_F, m_true_last = -CUDART_INF_F;
     const uint32_t s_addr = lane_base + L::COL_S0 + w * L::SW;
     const uint32_t cs_addr = s_addr + 128;  // c1_hi (8) | c1_lo (8)
 
-    int it = 0;
+    // persistent: this cluster's (head, query-pair) tiles; every barrier phase runs on the
+    // global block counter g = k*n + j (n is even, so block parity = warpgroup)
+    const int npq = n / 2, total = p.n_heads_flat * npq;
+    int it = 0;  // this warpgroup's block counter across tiles (= g >> 1)
+    int k = 0;
+    for (int u = cid; u < total; u += ncl, ++k) {
+    const int head = u / npq, qt = 2 * (u % npq) + static_cast<int>(rank);
+    const int seq_row0 = head * p.seq_len;
+    // own sums, referenced to m_ref (the reference max of this warpgroup's last block)
+    float l_w = 0.0f, lb_w = 0.0f, m_ref = -CUDART_INF_F, m_true_last = -CUDART_INF_F;
     for (int j = w; j < n; j += 2, ++it) {
+        const int g = k * n + j;
         if ((warp & 3) == 0) EFTA_TS(0, j);
         mbar_wait(&s_full[w], it & 1);
         if ((warp & 3) == 0) EFTA_TS(1, j);
         EFTA_TSQ(8, j);
         tc_fence_after();
-        const uint32_t pph = static_cast<uint32_t>((j - 1) >> 1) & 1u;  // partner's phase for block j-1
+        const uint32_t pph = static_cast<uint32_t>((g - 1) >> 1) & 1u;  // partner's phase for block g-1
         float pv[kBlock];
         float m_true_prev = -CUDART_INF_F, m_run_prev = -CUDART_INF_F;
         float m_true, m_new, bm, psum_f = 0.0f;
@@ -253,12 +261,12 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
 #pragma unroll
         for (int x = 0; x < 64; ++x) pk[x] = pack_half2(pv[2 * x], pv[2 * x + 1]);
         const bool need_o = j > 0 && !__all_sync(0xffffffffu, fo == 1.0f);
-        if (L::NPB == 1 ? (j > 0) : (j >= 2 || need_o)) {
+        if (L::NPB == 1 ? (g > 0) : (g >= 2 || need_o)) {
             if ((warp & 3) == 0) EFTA_TS(4, j);
             if (L::NPB == 1 || need_o)
-                mbar_wait(&o_done[1 - w], static_cast<uint32_t>((j - 1) >> 1) & 1u);
+                mbar_wait(&o_done[1 - w], static_cast<uint32_t>((g - 1) >> 1) & 1u);
             else
-                mbar_wait(&o_done[w], static_cast<uint32_t>((j - 2) >> 1) & 1u);
+                mbar_wait(&o_done[w], static_cast<uint32_t>((g - 2) >> 1) & 1u);
             if ((warp & 3) == 0) EFTA_TS(5, j);
             tc_fence_after();
         }
@@ -295,24 +303,24 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         m_true_last = m_true;
     }
 
-    // ------------------------------------------------ hand-over: warpgroup 1 -> 0
-    if (w == 1) {
+    // ------------------------------------------------ hand-over: warpgroup 0 -> 1
+    // Warpgroup 1 ran the tile's last block (n is even): it merges the sums and runs the
+    // epilogue while warpgroup 0 already starts the next tile.
+    if (w == 0) {
         xc->fin[row] = make_float4(l_w, lb_w, m_ref, m_true_last);
-        named_bar_arrive(kBarAltFin, 256);
-        return;
+        mbar_arrive(&fin_bar[wq]);
+        continue;
     }
-    named_bar_sync(kBarAltFin, 256);
+    mbar_wait(&fin_bar[wq], static_cast<uint32_t>(k) & 1u);
     const float4 fb = xc->fin[row];
-    const bool last_b = ((n - 1) & 1) != 0;
-    float m_run = last_b ? fb.z : m_ref;           // the chain's final reference max
-    const float m_true = last_b ? fb.w : m_true_last;
-    const float fa = ex2_approx((m_ref - m_run) * kLog2e);
+    float m_run = m_ref;  // the chain's final reference max (block n-1 is ours)
+    const float m_true = m_true_last;
     const float fbf = ex2_approx((fb.z - m_run) * kLog2e);
-    float l_run = __fadd_rn(__fmul_rn(l_w, fa), __fmul_rn(fb.x, fbf));
-    float lb = __fadd_rn(__fmul_rn(lb_w, fa), __fmul_rn(fb.y, fbf));
+    float l_run = __fadd_rn(l_w, __fmul_rn(fb.x, fbf));
+    float lb = __fadd_rn(lb_w, __fmul_rn(fb.y, fbf));
 
-    // ------------------------------------------------ epilogue (as row_wg, warpgroup 0 only)
-    mbar_wait(o_final, 0);
+    // ------------------------------------------------ epilogue (as row_wg, warpgroup 1)
+    mbar_wait(o_final, static_cast<uint32_t>(k) & 1u);
     tc_fence_after();
     float o[D];
     float c1[kStride], c2[kStride];
@@ -330,6 +338,10 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                          : 0.0f;
         }
     }
+    // O is in registers: the next tile's first P.V may overwrite the accumulator
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cluster(o_free, 0);
     {
         // bring O, its checksums, l and the lower bound from the lazy reference max to
         // the row's true max (the reference's final m); F == 1 for most rows
@@ -358,9 +370,9 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             l_run = lb;
             eps_mult = static_cast<double>(p.seq_len) / static_cast<double>(l_run);
         }
-        if (named_bar_or(7, 128, bad)) {
+        if (named_bar_or(7 + bo, 128, bad)) {
             if (row == 0) { rs.ints[0] = 0; rs.ints[1] = 0x7fffffff; rs.dbl[0] = 0.0; }
-            wg_sync();
+            wg_sync(bo);
             if (bad) {
                 atomicAdd(&rs.ints[0], 1);
                 atomicMin(&rs.ints[1], row);
@@ -372,13 +384,13 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                     old = atomicCAS(a, assumed, __double_as_longlong(viol));
                 } while (old != assumed);
             }
-            wg_sync();
+            wg_sync(bo);
             if (row == 0) {
                 atomicAdd(&p.counters->range_replacements, rs.ints[0]);
                 push_event(p, EFTA_ROWSUM_RANGE, head, qt, n, EFTA_CORRECTED, rs.ints[1], -1, 0, rs.ints[0], 0,
                            rs.dbl[0], 0.0);
             }
-            wg_sync();
+            wg_sync(bo);
         }
     }
     // normalization (efta.cpp:312-327): one IEEE reciprocal, then products (within 1 ulp of
@@ -394,26 +406,13 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
 #pragma unroll
         for (int x = 0; x < kStride; ++x) { c1[x] = __fmul_rn(c1[x], rl); c2[x] = __fmul_rn(c2[x], rl); }
         float res;
-        verify_output_tile<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res);
+        verify_output_tile<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res, bo);
         if (isfinite(res)) fam_out = fmaxf(fam_out, res);
     }
-    // store: the O tile is staged in the (now idle) K ring in the 128B-swizzled layout of the
-    // fp32 O map (D/32 boxes of 32 columns x 128 rows) and written with TMA bulk stores
-    // (one thread-owned 512-byte row per lane would otherwise be 32 strided 16-byte stores)
-#pragma unroll
-    for (int c = 0; c < D / 4; ++c) {
-        const int cb = c >> 3, k = c & 7;
-        *reinterpret_cast<float4*>(ostage + cb * 16384 + row * 128 + ((k ^ (row & 7)) << 4)) =
-            make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
-    }
-    fence_proxy_async_smem();
-    wg_sync();
-    if (row == 0) {
-#pragma unroll
-        for (int cb = 0; cb < D / 32; ++cb) tma_store_2d(tm_o, ostage + cb * 16384, cb * 32, seq_row0 + qt * kBlock);
-        bulk_commit_group();
-    }
     const size_t grow = static_cast<size_t>(seq_row0) + qt * kBlock + row;
+    float4* dst = reinterpret_cast<float4*>(p.o + grow * D);
+#pragma unroll
+    for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
     if (p.m_out) p.m_out[grow] = m_run;
     if (p.l_out) p.l_out[grow] = l_run;
     if (PROT) {
@@ -421,7 +420,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         for (int off = 16; off > 0; off >>= 1) fam_out = fmaxf(fam_out, __shfl_xor_sync(0xffffffffu, fam_out, off));
         if (lane == 0) atomic_max_nonneg(&p.counters->family_max[1], fam_out);
     }
-    if (row == 0) bulk_wait_group_read0();  // shared memory stays valid until the stores read it
+    }  // tiles
     (void)MODE;
 }
 

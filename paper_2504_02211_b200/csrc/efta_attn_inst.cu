@@ -1,3 +1,4 @@
+#include <algorithm>
 // efta_attn_inst.cu — instantiations of the fused attention kernel for one head
 // dim (EFTA_INST_D), all modes x {fast, debug/tap} variants.
 #include "efta_attn_kernel.cuh"
@@ -46,8 +47,8 @@ cudaError_t launch_d(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMa
 
 template <int D, int MODE>
 cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const CUtensorMap& tkb,
-                          const CUtensorMap& tkc, const CUtensorMap& tvt, const CUtensorMap& to,
-                          const AttnParams& p, int bh, cudaStream_t st) {
+                          const CUtensorMap& tkc, const CUtensorMap& tvt, const AttnParams& p, int bh,
+                          cudaStream_t st) {
     using PL = PairLayout<D, MODE != 0>;
     auto kern = efta_attn_pair_kernel<D, MODE>;
     static bool attr_set = false;
@@ -56,8 +57,16 @@ cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const C
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    dim3 grid(p.nblk, bh);
-    kern<<<grid, kPairThreads, PL::SMEM_BYTES, st>>>(tq, tka, tkb, tkc, tvt, to, p);
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int tiles = bh * (p.nblk / 2);  // (head, query pair) tiles
+    const int ncl = std::min(tiles, std::max(1, nsm / 2));
+    dim3 grid(2 * ncl);
+    kern<<<grid, kPairThreads, PL::SMEM_BYTES, st>>>(tq, tka, tkb, tkc, tvt, p);
     return cudaGetLastError();
 }
 
@@ -82,9 +91,9 @@ cudaError_t efta_launch_attn_d128(int mode, bool dbg, const CUtensorMap& tq, con
 #if EFTA_INST_D == 64
 cudaError_t efta_launch_attn_pair_d64(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                       const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
-                                      const CUtensorMap& to, const AttnParams& p, int bh, cudaStream_t st) {
-    return mode == 0 ? launch_pair_t<64, 0>(tq, tka, tkb, tkc, tvt, to, p, bh, st)
-                     : launch_pair_t<64, 2>(tq, tka, tkb, tkc, tvt, to, p, bh, st);
+                                      const AttnParams& p, int bh, cudaStream_t st) {
+    return mode == 0 ? launch_pair_t<64, 0>(tq, tka, tkb, tkc, tvt, p, bh, st)
+                     : launch_pair_t<64, 2>(tq, tka, tkb, tkc, tvt, p, bh, st);
 }
 cudaError_t efta_launch_encode_pair_d64(bool prot, const void* k, const void* v, void* kc, void* vt,
                                         int seq_len, int nblk, int bh, cudaStream_t st) {
@@ -100,9 +109,9 @@ cudaError_t efta_launch_encode_pair_d64(bool prot, const void* k, const void* v,
 #else
 cudaError_t efta_launch_attn_pair_d128(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                        const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
-                                       const CUtensorMap& to, const AttnParams& p, int bh, cudaStream_t st) {
-    return mode == 0 ? launch_pair_t<128, 0>(tq, tka, tkb, tkc, tvt, to, p, bh, st)
-                     : launch_pair_t<128, 2>(tq, tka, tkb, tkc, tvt, to, p, bh, st);
+                                       const AttnParams& p, int bh, cudaStream_t st) {
+    return mode == 0 ? launch_pair_t<128, 0>(tq, tka, tkb, tkc, tvt, p, bh, st)
+                     : launch_pair_t<128, 2>(tq, tka, tkb, tkc, tvt, p, bh, st);
 }
 cudaError_t efta_launch_encode_pair_d128(bool prot, const void* k, const void* v, void* kc, void* vt,
                                          int seq_len, int nblk, int bh, cudaStream_t st) {

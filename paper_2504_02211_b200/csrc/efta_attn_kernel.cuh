@@ -274,7 +274,8 @@ __device__ __forceinline__ void verify_output_tile(const AttnParams& p, float (&
                                                    const float (&c1)[kStride],
                                                    const float (&c2)[kStride], double eps_row,
                                                    int head, int bi, int bj, int row,
-                                                   const RowScratch& rs, float& residual_out) {
+                                                   const RowScratch& rs, float& residual_out,
+                                                   uint32_t bo = 0) {
     constexpr int G = D / kStride;
     float s1[kStride], s2[kStride];
     row_sums<D>(o, s1, s2);
@@ -290,8 +291,8 @@ __device__ __forceinline__ void verify_output_tile(const AttnParams& p, float (&
         viol |= (fabs(d1) > eps_row) || (fabs(d2) > eps_row * G);
     }
     residual_out = static_cast<float>(res);
-    const bool tile_cs_bad = named_bar_or(4, 128, cs_bad);
-    const bool any = named_bar_or(5, 128, viol || cs_bad);
+    const bool tile_cs_bad = named_bar_or(4 + bo, 128, cs_bad);
+    const bool any = named_bar_or(5 + bo, 128, viol || cs_bad);
     if (!any) return;
     RowVerify rv{};
     rv.best_col = -1;
@@ -309,7 +310,7 @@ __device__ __forceinline__ void verify_output_tile(const AttnParams& p, float (&
         for (int c = 0; c < D; ++c) o[c] = t[c];
         residual_out = static_cast<float>(rv.residual);
     }
-    TileReport tr = reduce_tile_report(rv, tile_cs_bad, row, rs.slots, rs.ints, rs.dbl);
+    TileReport tr = reduce_tile_report(rv, tile_cs_bad, row, rs.slots, rs.ints, rs.dbl, bo);
     if (row == 0)
         push_event(p, EFTA_OUTPUT_CHECKSUM, head, bi, bj, tr.status, tr.row, tr.col, tr.violations,
                    tr.corrections, tr.checksum_repair, tr.residual, tr.delta);

@@ -36,19 +36,21 @@ struct PairLayout {
     static constexpr int HN_S = SW / 2;                  // B rows per CTA, scores
     static constexpr int VROWS = PROT ? D + 32 : D;      // rows of the V^T (+VC^T) operand = O columns
     static constexpr int HN_V = VROWS / 2;               // B rows per CTA, P.V
-    static constexpr int KS = 4, VS = 4;
-    static constexpr uint32_t Q_BYTES = NSUB * 16384;
+    // 4-stage K / V rings, 3 where the double-buffered Q would not fit (protected d=128)
+    static constexpr int KS = (D == 128 && PROT) ? 3 : 4, VS = KS;
+    static constexpr uint32_t Q_BYTES = NSUB * 16384;  // one Q buffer (two: the next tile's Q loads early)
     static constexpr uint32_t K_CHUNK = HN_S * 128;      // one 64-column chunk of the K half
     static constexpr uint32_t K_STAGE = NSUB * K_CHUNK;
     static constexpr uint32_t V_CHUNK = HN_V * 128;      // one 64-key chunk of the V^T half
     static constexpr uint32_t V_STAGE = 2 * V_CHUNK;
     static constexpr uint32_t OFF_Q = 0;
-    static constexpr uint32_t OFF_K = OFF_Q + Q_BYTES;
+    static constexpr uint32_t OFF_K = OFF_Q + 2 * Q_BYTES;
     static constexpr uint32_t OFF_V = OFF_K + KS * K_STAGE;
     static constexpr uint32_t OFF_BAR = OFF_V + VS * V_STAGE;
     // q_full, k_full/empty[KS], v_full/empty[VS], s_full[2], s_free[2], p_ready[2],
-    // o_done[2], o_final, chain barriers mx_early[2][4], mx_late[2][4]
-    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2 + 2 + 2 + 1 + 16;
+    // o_done[2], o_final, chain barriers mx_early[2][4], mx_late[2][4], q_empty[2], o_free, fin[4],
+    // second q_full
+    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2 + 2 + 2 + 1 + 16 + 2 + 1 + 4 + 1;
     static constexpr uint32_t OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
     static constexpr uint32_t RED_BYTES = 128 * 24 + 256;  // per row warpgroup
@@ -63,7 +65,6 @@ struct PairLayout {
     static_assert(K_CHUNK % 1024 == 0 && V_CHUNK % 1024 == 0, "swizzle atoms must stay 1 KB aligned");
     static_assert(RED_BYTES == AttnLayout<D>::RED_BYTES, "row scratch size");
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
-    static_assert(KS * K_STAGE >= D * 128 * 4, "the epilogue stages the fp32 O tile in the idle K ring");
 };
 constexpr int kPairThreads = 384;  // warps 0-3: TMA K / score MMA / P.V MMA / TMA Q,V; 4-7, 8-11: row warpgroups
 
@@ -128,8 +129,7 @@ template <int D, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_ka,
                       const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_kc,
-                      const __grid_constant__ CUtensorMap tm_vt, const __grid_constant__ CUtensorMap tm_o,
-                      const AttnParams p) {
+                      const __grid_constant__ CUtensorMap tm_vt, const AttnParams p) {
     constexpr bool PROT = MODE != EFTA_MODE_NONE;
     using L = PairLayout<D, PROT>;
     constexpr int KS = L::KS, VS = L::VS, NSUB = L::NSUB;
@@ -149,12 +149,18 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     uint64_t* o_final = o_done + 2;
     uint64_t* mx_early = o_final + 1;  // [2][4]
     uint64_t* mx_late = mx_early + 8;  // [2][4]
+    uint64_t* q_empty = mx_late + 8;   // [2] every score MMA of the tile using Q buffer b done
+    uint64_t* o_free = q_empty + 2;    // the epilogue read O (leader; 4 warps x 2 CTAs)
+    uint64_t* fin_bar = o_free + 1;    // [4] warpgroup 0's sums of the tile (per warp quarter)
+    uint64_t* q_full2 = fin_bar + 4;   // q_full of Q buffer 1 (q_full is buffer 0's)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
     const int warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_rank();
-    const int qt = blockIdx.x, head = blockIdx.y, n = p.nblk;
-    const int seq_row0 = head * p.seq_len;
+    const int n = p.nblk;
+    // persistent clusters: tile u = (head, query pair) for u = cid, cid + ncl, ...
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int npq = n / 2, total = p.n_heads_flat * npq;
 
     if (warp == 0 && lane == 0) {
         mbar_init(q_full, 1);
@@ -168,6 +174,11 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         }
         mbar_init(o_final, 1);
         for (int i = 0; i < 16; ++i) mbar_init(&mx_early[i], 32);
+        mbar_init(&q_empty[0], 1);
+        mbar_init(&q_empty[1], 1);
+        mbar_init(q_full2, 1);
+        mbar_init(o_free, 8);
+        for (int i = 0; i < 4; ++i) mbar_init(&fin_bar[i], 32);
         fence_barrier_init();
         tma_prefetch_desc(&tm_q);
         tma_prefetch_desc(&tm_ka);
@@ -188,24 +199,30 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         // -------------------------------------------------------- K (+KC1) half producer
         setmaxnreg_dec<40>();
         if (lane == 0) {
-            for (int j = 0; j < n; ++j) {
-                const int s = j % KS;
-                mbar_wait(&k_empty[s], ((j / KS) & 1) ^ 1);
-                uint8_t* dst = smem + L::OFF_K + s * L::K_STAGE;
-                if (rank == 0) mbar_arrive_expect_tx(&k_full[s], 2 * L::K_STAGE);
-                const int krow = seq_row0 + j * kBlock;
-                const int crow = (head * n + j) * 32;
+            int g = 0;
+            for (int u = cid; u < total; u += ncl) {
+                const int head = u / npq;
+                const int seq_row0 = head * p.seq_len;
+                for (int j = 0; j < n; ++j, ++g) {
+                    const int s = g % KS;
+                    mbar_wait(&k_empty[s], ((g / KS) & 1) ^ 1);
+                    uint8_t* dst = smem + L::OFF_K + s * L::K_STAGE;
+                    if (rank == 0) mbar_arrive_expect_tx(&k_full[s], 2 * L::K_STAGE);
+                    const int krow = seq_row0 + j * kBlock;
+                    const int crow = (head * n + j) * 32;
 #pragma unroll
-                for (int sub = 0; sub < NSUB; ++sub) {
-                    uint8_t* c = dst + sub * L::K_CHUNK;
-                    if (!PROT) {
-                        tma_load_2d_pair(c, &tm_ka, &k_full[s], sub * 64, krow + 64 * rank, kEvictLast);
-                    } else if (rank == 0) {
-                        tma_load_2d_pair(c, &tm_ka, &k_full[s], sub * 64, krow, kEvictLast);
-                    } else {
-                        tma_load_2d_pair(c, &tm_kb, &k_full[s], sub * 64, krow + 72, kEvictLast);
-                        tma_load_2d_pair(c + 56 * 128, &tm_kc, &k_full[s], sub * 64, crow, kEvictLast);       // c1_hi
-                        tma_load_2d_pair(c + 64 * 128, &tm_kc, &k_full[s], sub * 64, crow + 16, kEvictLast);  // c1_lo
+                    for (int sub = 0; sub < NSUB; ++sub) {
+                        uint8_t* c = dst + sub * L::K_CHUNK;
+                        if (!PROT) {
+                            tma_load_2d_pair(c, &tm_ka, &k_full[s], sub * 64, krow + 64 * rank, kEvictLast);
+                        } else if (rank == 0) {
+                            tma_load_2d_pair(c, &tm_ka, &k_full[s], sub * 64, krow, kEvictLast);
+                        } else {
+                            tma_load_2d_pair(c, &tm_kb, &k_full[s], sub * 64, krow + 72, kEvictLast);
+                            tma_load_2d_pair(c + 56 * 128, &tm_kc, &k_full[s], sub * 64, crow, kEvictLast);  // c1_hi
+                            tma_load_2d_pair(c + 64 * 128, &tm_kc, &k_full[s], sub * 64, crow + 16,
+                                             kEvictLast);  // c1_lo
+                        }
                     }
                 }
             }
@@ -214,20 +231,29 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         // -------------------------------------------------------- Q, V^T (+VC^T) half producer
         setmaxnreg_dec<40>();
         if (lane == 0) {
-            if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * L::Q_BYTES);
+            int g = 0, k = 0;
+            for (int u = cid; u < total; u += ncl, ++k) {
+                const int head = u / npq, qt = 2 * (u % npq) + static_cast<int>(rank);
+                const int seq_row0 = head * p.seq_len;
+                // Q buffer k&1 was last read by the score MMAs of tile k-2
+                const int qb = k & 1;
+                uint64_t* qf = qb ? q_full2 : q_full;
+                if (k >= 2) mbar_wait(&q_empty[qb], ((k - 2) >> 1) & 1);
+                if (rank == 0) mbar_arrive_expect_tx(qf, 2 * L::Q_BYTES);
 #pragma unroll
-            for (int sub = 0; sub < NSUB; ++sub)
-                tma_load_2d_pair(smem + L::OFF_Q + sub * 16384, &tm_q, q_full, sub * 64, seq_row0 + qt * kBlock,
-                                 kEvictFirst);
-            for (int j = 0; j < n; ++j) {
-                const int s = j % VS;
-                mbar_wait(&v_empty[s], ((j / VS) & 1) ^ 1);
-                uint8_t* dst = smem + L::OFF_V + s * L::V_STAGE;
-                if (rank == 0) mbar_arrive_expect_tx(&v_full[s], 2 * L::V_STAGE);
-                const int vrow = (head * n + j) * L::VROWS + L::HN_V * rank;
+                for (int sub = 0; sub < NSUB; ++sub)
+                    tma_load_2d_pair(smem + L::OFF_Q + qb * L::Q_BYTES + sub * 16384, &tm_q, qf, sub * 64,
+                                     seq_row0 + qt * kBlock, kEvictFirst);
+                for (int j = 0; j < n; ++j, ++g) {
+                    const int s = g % VS;
+                    mbar_wait(&v_empty[s], ((g / VS) & 1) ^ 1);
+                    uint8_t* dst = smem + L::OFF_V + s * L::V_STAGE;
+                    if (rank == 0) mbar_arrive_expect_tx(&v_full[s], 2 * L::V_STAGE);
+                    const int vrow = (head * n + j) * L::VROWS + L::HN_V * rank;
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
-                    tma_load_2d_pair(dst + c * L::V_CHUNK, &tm_vt, &v_full[s], c * 64, vrow, kEvictLast);
+                    for (int c = 0; c < 2; ++c)
+                        tma_load_2d_pair(dst + c * L::V_CHUNK, &tm_vt, &v_full[s], c * 64, vrow, kEvictLast);
+                }
             }
         }
     } else if (warp == 1) {
@@ -240,30 +266,36 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             constexpr uint32_t ID_S = idesc_f16_f32(256, L::SW, 0, 0);
             const uint64_t dq = smem_desc_sw128(q_smem, 16, 1024);
             const uint64_t dk0 = smem_desc_sw128(k_smem, 16, 1024);
-            mbar_wait(q_full, 0);
-            tc_fence_after();
-            for (int j = 0; j < n; ++j) {
-                if (j >= 2) {
-                    mbar_wait(&s_free[j & 1], ((j - 2) >> 1) & 1);
-                    EFTA_TS(7, j - 2);
-                }
-                const int s = j % KS;
-                mbar_wait(&k_full[s], (j / KS) & 1);
+            int g = 0, k = 0;
+            for (int u = cid; u < total; u += ncl, ++k) {
+                const int qb = k & 1;
+                mbar_wait(qb ? q_full2 : q_full, (k >> 1) & 1);
                 tc_fence_after();
-                const uint64_t dk = dk0 + ((s * L::K_STAGE) >> 4);
-                const uint32_t d_s = tmem + L::COL_S0 + (j & 1) * L::SW;
-                if (elect_one()) {
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t offq = (kk >> 2) * 16384 + (kk & 3) * 32;
-                        const uint32_t offk = (kk >> 2) * L::K_CHUNK + (kk & 3) * 32;
-                        mma2_ss(d_s, dq + (offq >> 4), dk + (offk >> 4), ID_S, kk > 0);
+                const uint64_t dqb = dq + ((qb * L::Q_BYTES) >> 4);
+                for (int j = 0; j < n; ++j, ++g) {
+                    if (g >= 2) {
+                        mbar_wait(&s_free[g & 1], ((g - 2) >> 1) & 1);
+                        EFTA_TS(7, j - 2);
                     }
-                    commit2_both(&k_empty[s]);
-                    commit2_both(&s_full[j & 1]);
+                    const int s = g % KS;
+                    mbar_wait(&k_full[s], (g / KS) & 1);
+                    tc_fence_after();
+                    const uint64_t dk = dk0 + ((s * L::K_STAGE) >> 4);
+                    const uint32_t d_s = tmem + L::COL_S0 + (g & 1) * L::SW;
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t offq = (kk >> 2) * 16384 + (kk & 3) * 32;
+                            const uint32_t offk = (kk >> 2) * L::K_CHUNK + (kk & 3) * 32;
+                            mma2_ss(d_s, dqb + (offq >> 4), dk + (offk >> 4), ID_S, kk > 0);
+                        }
+                        commit2_both(&k_empty[s]);
+                        commit2_both(&s_full[g & 1]);
+                        if (j == n - 1) commit2_both(&q_empty[qb]);
+                    }
+                    __syncwarp();
+                    EFTA_TS(11, j - 2);
                 }
-                __syncwarp();
-                EFTA_TS(11, j - 2);
             }
         }
     } else if (warp == 2) {
@@ -273,37 +305,41 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             constexpr uint32_t ID_PV = idesc_f16_f32(256, L::VROWS, 0, 0);
             const uint64_t dv0 = smem_desc_sw128(v_smem, 16, 1024);
             const uint32_t d_o = tmem + L::COL_O;
-            for (int j = 0; j < n; ++j) {
-                EFTA_TS(10, j);
-                mbar_wait(&p_ready[j & 1], (j >> 1) & 1);
-                EFTA_TS(12, j);
-                tc_fence_after();
-                const int s = j % VS;
-                mbar_wait(&v_full[s], (j / VS) & 1);
-                EFTA_TS(14, j);
-                tc_fence_after();
-                const uint64_t dv = dv0 + ((s * L::V_STAGE) >> 4);
-                const uint32_t a_p = tmem + L::COL_P + (L::NPB == 2 ? (j & 1) * 64 : 0);
-                if (elect_one()) {
+            int g = 0, k = 0;
+            for (int u = cid; u < total; u += ncl, ++k) {
+                for (int j = 0; j < n; ++j, ++g) {
+                    EFTA_TS(10, j);
+                    mbar_wait(&p_ready[g & 1], (g >> 1) & 1);
+                    EFTA_TS(12, j);
+                    tc_fence_after();
+                    const int s = g % VS;
+                    mbar_wait(&v_full[s], (g / VS) & 1);
+                    EFTA_TS(14, j);
+                    if (j == 0 && k > 0) mbar_wait(o_free, (k - 1) & 1);  // the last epilogue read O
+                    tc_fence_after();
+                    const uint64_t dv = dv0 + ((s * L::V_STAGE) >> 4);
+                    const uint32_t a_p = tmem + L::COL_P + (L::NPB == 2 ? (g & 1) * 64 : 0);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < kBlock / 16; ++kk) {
-                        const uint32_t offv = (kk >> 2) * L::V_CHUNK + (kk & 3) * 32;
-                        mma2_ts(d_o, a_p + kk * 8, dv + (offv >> 4), ID_PV, (j > 0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < kBlock / 16; ++kk) {
+                            const uint32_t offv = (kk >> 2) * L::V_CHUNK + (kk & 3) * 32;
+                            mma2_ts(d_o, a_p + kk * 8, dv + (offv >> 4), ID_PV, (j > 0 || kk > 0) ? 1u : 0u);
+                        }
+                        commit2_both(&v_empty[s]);
+                        commit2_both(&o_done[g & 1]);
+                        if (j == n - 1) commit2_both(o_final);
                     }
-                    commit2_both(&v_empty[s]);
-                    commit2_both(&o_done[j & 1]);
-                    if (j == n - 1) commit2_both(o_final);
+                    __syncwarp();
+                    EFTA_TS(13, j);
                 }
-                __syncwarp();
-                EFTA_TS(13, j);
             }
         }
         __syncwarp();
     } else {
         setmaxnreg_inc<232>();
         row_alt<D, PROT>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH), s_full, s_free,
-                         p_ready, o_done, o_final, mx_early, mx_late, tmem, warp, lane, head, qt, n, seq_row0,
-                         &tm_o, smem + L::OFF_K);
+                         p_ready, o_done, o_final, mx_early, mx_late, fin_bar, o_free, tmem, warp, lane, n, cid,
+                         ncl, rank);
     }
 
     tc_fence_before();

@@ -68,20 +68,6 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 2D fp32 tensor [rows, cols] row-major, box {32, box_rows} (128 B inner), 128B swizzle:
-// the pair kernel's O tile, staged in shared memory and written with TMA stores.
-bool make_map_f32(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
-    EncodeTiledFn fn = encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[2] = {cols, rows};
-    cuuint64_t strides[1] = {cols * 4};
-    cuuint32_t box[2] = {32, box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
-              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 int validate(const efta_attn_desc* d) {
     if (!d) return fail(1, "efta: null descriptor");
     // reference AttnConfig::validate (include/efta/config.hpp:30-41)
@@ -202,7 +188,7 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     char* wsb = static_cast<char*>(workspace);
     uint16_t* kc = wsb ? reinterpret_cast<uint16_t*>(wsb + wl.kc) : nullptr;
     uint16_t* r2 = wsb ? reinterpret_cast<uint16_t*>(wsb + wl.r2) : nullptr;
-    CUtensorMap tq, tk, tv, tkc, tvc, to;
+    CUtensorMap tq, tk, tv, tkc, tvc;
     const uint64_t rows = static_cast<uint64_t>(bh) * d->seq_len;
     bool ok;
     if (pair) {
@@ -216,7 +202,6 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
         // score operand N = 144 (protected: K + c1_hi + c1_lo rows) or 128, half per CTA:
         // leader K rows 0..71 (0..63), peer K rows 72..127 + two 8-row KC boxes (64..127)
         ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, rows, D, prot ? 72 : 64) &&
-             make_map_f32(&to, o, rows, D, 128) &&
              make_map(&tvc, r2, static_cast<uint64_t>(bh) * nblk * vrows, 128, vrows / 2);
         if (prot)
             ok = ok && make_map(&tv, k, rows, D, 56) &&
@@ -279,8 +264,8 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     const bool dbg = d->debug != 0;
     cudaError_t e;
     if (pair)  // maps: q, K half A, K half B (protected peer), KC, [V^T ; VC^T]
-        e = (D == 64) ? efta_launch_attn_pair_d64(d->mode, tq, tk, tv, tkc, tvc, to, p, bh, st)
-                      : efta_launch_attn_pair_d128(d->mode, tq, tk, tv, tkc, tvc, to, p, bh, st);
+        e = (D == 64) ? efta_launch_attn_pair_d64(d->mode, tq, tk, tv, tkc, tvc, p, bh, st)
+                      : efta_launch_attn_pair_d128(d->mode, tq, tk, tv, tkc, tvc, p, bh, st);
     else
         e = (D == 64) ? efta_launch_attn_d64(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st)
                       : efta_launch_attn_d128(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);

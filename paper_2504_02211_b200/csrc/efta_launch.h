@@ -19,13 +19,14 @@ cudaError_t efta_launch_attn_d128(int mode, bool dbg, const CUtensorMap& tq, con
 void efta_internal_set_error(const char* msg);
 
 // CTA-pair (cta_group::2) fast path: modes NONE / EFTA_OPT, even number of query tiles.
-// maps: q, k half A, k half B (protected peer), kc, [V^T; VC^T], o (fp32, TMA store).
+// maps: q, k half A, k half B (protected peer), kc, [V^T; VC^T]. Persistent: one cluster
+// (CTA pair) per two SMs loops over the (head, query pair) tiles.
 cudaError_t efta_launch_attn_pair_d64(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                       const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
-                                      const CUtensorMap& to, const efta_sm100::AttnParams& p, int bh, cudaStream_t st);
+                                      const efta_sm100::AttnParams& p, int bh, cudaStream_t st);
 cudaError_t efta_launch_attn_pair_d128(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                        const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
-                                       const CUtensorMap& to, const efta_sm100::AttnParams& p, int bh, cudaStream_t st);
+                                       const efta_sm100::AttnParams& p, int bh, cudaStream_t st);
 cudaError_t efta_launch_encode_pair_d64(bool prot, const void* k, const void* v, void* kc, void* vt,
                                         int seq_len, int nblk, int bh, cudaStream_t st);
 cudaError_t efta_launch_encode_pair_d128(bool prot, const void* k, const void* v, void* kc, void* vt,
