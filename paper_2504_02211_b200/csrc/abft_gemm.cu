@@ -16,7 +16,10 @@
 //   [W rows 128..255| Wc_lo rows 0..15] -> TMEM cols [144, 288)
 // so A is read twice per k-step and the checksum work is 32/256 = 12.5% extra MMA.
 // Persistent grid (one CTA per SM), static round-robin tile order (m-major rows of
-// n-tiles so consecutive CTAs share X rows in L2).
+// n-tiles so consecutive CTAs share X rows in L2). The single 288-column accumulator is
+// drained by 8 epilogue warps: warps 4-7 own output columns 0..127 of their rows, warps
+// 8-11 columns 128..255 (same TMEM lanes); the upper half hands its partial strided sums
+// (groups l = 16..31) to the lower half through shared memory, which verifies the row.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -41,7 +44,9 @@ constexpr uint32_t STAGE = A_BYTES + B_BYTES;
 constexpr uint32_t OFF_BAR = STAGES * STAGE;
 constexpr uint32_t OFF_TMEM = OFF_BAR + (2 * STAGES + 2) * 8;
 constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
-constexpr uint32_t SMEM_BYTES = OFF_RED + 128 * 24 + 256 + 1024;
+constexpr uint32_t OFF_XS = OFF_RED + 128 * 24 + 256;  // column half 1's partial strided sums [128][16]
+constexpr uint32_t SMEM_BYTES = OFF_XS + 128 * 16 * 4 + 1024;
+constexpr int GEMM_THREADS = 384;  // warps 0-3: TMA / MMA / idle / idle; 4-11: epilogue (2 column halves)
 
 struct GemmParams {
     int m, n, k, m_tiles, n_tiles, k_chunks;
@@ -61,7 +66,7 @@ struct RowScratchG {
 };
 
 template <bool DBG>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
 abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                  const __grid_constant__ CUtensorMap tm_wc, const GemmParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -77,7 +82,7 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         mbar_init(tfull, 1);
-        mbar_init(tempty, 128);
+        mbar_init(tempty, 256);
         fence_barrier_init();
         tma_prefetch_desc(&tm_x);
         tma_prefetch_desc(&tm_w);
@@ -90,6 +95,7 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
+        setmaxnreg_dec<40>();
         if (lane == 0) {  // ------------------------------------------ TMA producer
             int it = 0;
             for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
@@ -109,39 +115,46 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ------------------------------------------ MMA issuer
-            constexpr uint32_t ID = idesc_f16_f32(128, 144, 0, 0);
-            const uint32_t sbase = smem_u32(smem);
-            int it = 0, tl = 0;
-            for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
-                mbar_wait(tempty, (tl & 1) ^ 1);  // epilogue drained the accumulator
+        // ------------------------------------------------------------- MMA issuer
+        // converged warp, one elected lane issues (descriptors stay in uniform registers)
+        setmaxnreg_dec<40>();
+        constexpr uint32_t ID = idesc_f16_f32(128, 144, 0, 0);
+        const uint64_t d0 = smem_desc_sw128(smem_u32(smem), 16, 1024);
+        int it = 0, tl = 0;
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
+            mbar_wait(tempty, (tl & 1) ^ 1);  // epilogue drained the accumulator
+            tc_fence_after();
+            for (int kc = 0; kc < p.k_chunks; ++kc, ++it) {
+                const int s = it % STAGES;
+                mbar_wait(&full[s], (it / STAGES) & 1);
                 tc_fence_after();
-                for (int kc = 0; kc < p.k_chunks; ++kc, ++it) {
-                    const int s = it % STAGES;
-                    mbar_wait(&full[s], (it / STAGES) & 1);
-                    tc_fence_after();
-                    const uint32_t a = sbase + s * STAGE, b = a + A_BYTES;
+                const uint64_t ad = d0 + ((s * STAGE) >> 4), bd = ad + (A_BYTES >> 4);
+                if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < GK / 16; ++kk) {
-                        const uint64_t ad = smem_desc_sw128(a + kk * 32, 16, 1024);
                         const uint32_t acc = (kc | kk) > 0;
-                        mma_ss(tmem, ad, smem_desc_sw128(b + kk * 32, 16, 1024), ID, acc);
-                        mma_ss(tmem + 144, ad, smem_desc_sw128(b + B_HALF + kk * 32, 16, 1024), ID, acc);
+                        mma_ss(tmem, ad + kk * 2, bd + kk * 2, ID, acc);
+                        mma_ss(tmem + 144, ad + kk * 2, bd + (B_HALF >> 4) + kk * 2, ID, acc);
                     }
                     tc_commit(&empty[s]);
                 }
-                tc_commit(tfull);
+                __syncwarp();
             }
+            if (elect_one()) tc_commit(tfull);
+            __syncwarp();
         }
-        __syncwarp();
-    } else if (warp >= 4) {
-        // ------------------------------------------------------- epilogue (thread = row)
-        const int wq = warp - 4, row = wq * 32 + lane;
+    } else if (warp < 4) {
+        setmaxnreg_dec<40>();
+    } else {
+        // ------------------------------------------------------- epilogue (thread = row, column half)
+        setmaxnreg_inc<232>();
+        const int wq = warp & 3, row = wq * 32 + lane, half = (warp - 4) >> 2;
         const uint32_t lb = tmem + (static_cast<uint32_t>(wq * 32) << 16);
         RowScratchG rs;
         rs.slots = reinterpret_cast<RowSlot*>(smem + OFF_RED);
         rs.ints = reinterpret_cast<int*>(smem + OFF_RED + 128 * sizeof(RowSlot));
         rs.dbl = reinterpret_cast<double*>(smem + OFF_RED + 128 * sizeof(RowSlot) + 16 * sizeof(int));
+        float* xs = reinterpret_cast<float*>(smem + OFF_XS) + row * 16;
         float fam = 0.0f;
         int tl = 0;
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
@@ -163,7 +176,7 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
             __half* yrow = p.y + static_cast<size_t>(grow) * p.n + nt * GN;
             bool nonfin = false;
 #pragma unroll 1
-            for (int c = 0; c < 8; ++c) {
+            for (int c = half * 4; c < half * 4 + 4; ++c) {
                 float v[32];
                 tmem_ld32(lb + (c < 4 ? c * 32 : 144 + (c - 4) * 32), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
                 tmem_wait_ld();
@@ -190,6 +203,22 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                 uint4* dst = reinterpret_cast<uint4*>(yrow + c * 32);
 #pragma unroll
                 for (int x = 0; x < 4; ++x) dst[x] = pk[x];
+            }
+            if (half == 1) {
+                // hand the partial sums of groups l = 16..31 to the lower half; its verdict
+                // (and any correction) follows from the still-resident accumulator
+#pragma unroll
+                for (int x = 0; x < 8; ++x) { xs[x] = s1[x]; xs[8 + x] = s2[x]; }
+                named_bar_arrive(6, 256);
+                tc_fence_before();
+                mbar_arrive(tempty);
+                continue;
+            }
+            named_bar_sync(6, 256);
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                s1[x] = __fadd_rn(s1[x], xs[x]);
+                s2[x] = __fadd_rn(s2[x], xs[8 + x]);
             }
             uint32_t hi[16], lo[16];
             tmem_ld16(lb + 128, hi);
@@ -392,7 +421,7 @@ int efta_abft_gemm_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_
     auto launch = [&](auto kern) -> cudaError_t {
         cudaError_t ee = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
         if (ee != cudaSuccess) return ee;
-        kern<<<grid, 256, SMEM_BYTES, st>>>(tx, tw, twc, p);
+        kern<<<grid, GEMM_THREADS, SMEM_BYTES, st>>>(tx, tw, twc, p);
         return cudaGetLastError();
     };
     e = d->debug ? launch(abft_gemm_kernel<true>) : launch(abft_gemm_kernel<false>);
