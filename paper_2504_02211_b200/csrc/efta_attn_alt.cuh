@@ -51,8 +51,8 @@ template <int D, bool PROT>
 __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, uint64_t* s_full,
                                         uint64_t* s_free, uint64_t* p_ready, uint64_t* o_done, uint64_t* o_final,
                                         uint64_t* mx_early, uint64_t* mx_late, uint64_t* fin_bar,
-                                        uint64_t* o_free, uint32_t tmem, int warp, int lane, int n, int cid,
-                                        int ncl, uint32_t rank) {
+                                        uint64_t* o_free, uint32_t tmem, int warp, int lane, int n,
+                                        const int* tinfo, uint64_t* t_full, uint64_t* t_empty, uint32_t rank) {
     using L = PairLayout<D, PROT>;
     constexpr int MODE = PROT ? EFTA_MODE_EFTA_OPT : EFTA_MODE_NONE;
     const int w = (warp - 4) >> 2;
@@ -76,12 +76,13 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     const uint32_t s_addr = lane_base + L::COL_S0 + w * L::SW;
     const uint32_t cs_addr = s_addr + 128;  // c1_hi (8) | c1_lo (8)
 
-    // persistent: this cluster's (head, query-pair) tiles; every barrier phase runs on the
+    // persistent: the (head, query-pair) tiles this cluster draws from the tile ring; every barrier phase runs on the
     // global block counter g = k*n + j (n is even, so block parity = warpgroup)
-    const int npq = n / 2, total = p.n_heads_flat * npq;
+    const int npq = n / 2;
     int it = 0;  // this warpgroup's block counter across tiles (= g >> 1)
-    int k = 0;
-    for (int u = cid; u < total; u += ncl, ++k) {
+    for (int k = 0;; ++k) {
+    const int u = pair_next_tile(tinfo, t_full, t_empty, k, true);
+    if (u < 0) break;
     const int head = u / npq, qt = 2 * (u % npq) + static_cast<int>(rank);
     const int seq_row0 = head * p.seq_len;
     // own sums, referenced to m_ref (the reference max of this warpgroup's last block)

@@ -49,13 +49,14 @@ struct PairLayout {
     static constexpr uint32_t OFF_BAR = OFF_V + VS * V_STAGE;
     // q_full, k_full/empty[KS], v_full/empty[VS], s_full[2], s_free[2], p_ready[2],
     // o_done[2], o_final, chain barriers mx_early[2][4], mx_late[2][4], q_empty[2], o_free, fin[4],
-    // second q_full
-    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2 + 2 + 2 + 1 + 16 + 2 + 1 + 4 + 1;
+    // second q_full, tile ring full[4] / empty[4]
+    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2 + 2 + 2 + 1 + 16 + 2 + 1 + 4 + 1 + 8;
     static constexpr uint32_t OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
     static constexpr uint32_t RED_BYTES = 128 * 24 + 256;  // per row warpgroup
     static constexpr uint32_t OFF_XCH = OFF_RED + 2 * RED_BYTES;
-    static constexpr uint32_t SMEM_BYTES = OFF_XCH + 6144 + 1024;
+    static constexpr uint32_t OFF_TINFO = OFF_XCH + 6144;  // tile ring: int[4]
+    static constexpr uint32_t SMEM_BYTES = OFF_TINFO + 16 + 1024;
     // TMEM columns
     static constexpr uint32_t COL_S0 = 0, COL_O = 2 * SW, COL_P = COL_O + VROWS, TMEM_COLS = 512;
     // one P buffer per row warpgroup when it fits (unprotected d=128, every d=64 variant);
@@ -67,6 +68,49 @@ struct PairLayout {
     static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
 constexpr int kPairThreads = 384;  // warps 0-3: TMA K / score MMA / P.V MMA / TMA Q,V; 4-7, 8-11: row warpgroups
+
+// ---- dynamic tile schedule: an in-order atomic tile counter, fetched one tile ahead by the
+// leader's Q/V producer and broadcast to both CTAs through a 4-slot ring (keeps the set of
+// heads in flight compact, so the K/V blocks of a head are read from HBM once: a static
+// round-robin schedule lets clusters drift apart and spread over more heads than L2 holds)
+constexpr int kTileRing = 4;
+constexpr int kTileConsumers = 21;  // leader warps 0,1,2,4-11 + peer warps 0,3,4-11
+__device__ __forceinline__ void st_cluster_s32(const void* smem_local, uint32_t cta, int v) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.s32 [ra], %2;\n\t}" ::"r"(
+            smem_u32(smem_local)),
+        "r"(cta), "r"(v)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_rel_cluster(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+// consumer side: tile of this cluster's k-th step (-1: done); one arrival per calling warp
+__device__ __forceinline__ int pair_next_tile(const int* tinfo, uint64_t* tfull, uint64_t* tempty, int k,
+                                              bool warp_wide) {
+    const int slot = k & (kTileRing - 1);
+    mbar_wait_acq_cluster(&tfull[slot], static_cast<uint32_t>(k / kTileRing) & 1u);
+    const int u = *reinterpret_cast<const volatile int*>(&tinfo[slot]);
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || (threadIdx.x & 31) == 0) mbar_arrive_rel_cluster(&tempty[slot], 0);
+    return u;
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -153,14 +197,17 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     uint64_t* o_free = q_empty + 2;    // the epilogue read O (leader; 4 warps x 2 CTAs)
     uint64_t* fin_bar = o_free + 1;    // [4] warpgroup 0's sums of the tile (per warp quarter)
     uint64_t* q_full2 = fin_bar + 4;   // q_full of Q buffer 1 (q_full is buffer 0's)
+    uint64_t* t_full = q_full2 + 1;    // [4] tile ring slot published (this CTA)
+    uint64_t* t_empty = t_full + 4;    // [4] tile ring slot consumed by all 21 warps (leader)
+    int* tinfo = reinterpret_cast<int*>(smem + L::OFF_TINFO);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
     const int warp = warp_id(), lane = lane_id();
     const uint32_t rank = cluster_rank();
     const int n = p.nblk;
-    // persistent clusters: tile u = (head, query pair) for u = cid, cid + ncl, ...
-    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    // persistent clusters: tile u = (head, query pair), handed out in order by an atomic counter
     const int npq = n / 2, total = p.n_heads_flat * npq;
+    int* tile_counter = reinterpret_cast<int*>(p.scratch);  // zeroed by the host before the launch
 
     if (warp == 0 && lane == 0) {
         mbar_init(q_full, 1);
@@ -177,6 +224,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         mbar_init(&q_empty[0], 1);
         mbar_init(&q_empty[1], 1);
         mbar_init(q_full2, 1);
+        for (int i = 0; i < kTileRing; ++i) { mbar_init(&t_full[i], 1); mbar_init(&t_empty[i], kTileConsumers); }
         mbar_init(o_free, 8);
         for (int i = 0; i < 4; ++i) mbar_init(&fin_bar[i], 32);
         fence_barrier_init();
@@ -200,7 +248,9 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         setmaxnreg_dec<40>();
         if (lane == 0) {
             int g = 0;
-            for (int u = cid; u < total; u += ncl) {
+            for (int k = 0;; ++k) {
+                const int u = pair_next_tile(tinfo, t_full, t_empty, k, false);
+                if (u < 0) break;
                 const int head = u / npq;
                 const int seq_row0 = head * p.seq_len;
                 for (int j = 0; j < n; ++j, ++g) {
@@ -231,8 +281,36 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         // -------------------------------------------------------- Q, V^T (+VC^T) half producer
         setmaxnreg_dec<40>();
         if (lane == 0) {
-            int g = 0, k = 0;
-            for (int u = cid; u < total; u += ncl, ++k) {
+            // leader: fetch tiles in order, one ahead, and publish them to both CTAs
+            auto publish = [&](int k, int u) {
+                const int slot = k & (kTileRing - 1);
+                mbar_wait_acq_cluster(&t_empty[slot], (static_cast<uint32_t>(k / kTileRing) & 1u) ^ 1u);
+                tinfo[slot] = u;
+                st_cluster_s32(&tinfo[slot], 1, u);
+                mbar_arrive_rel_cluster(&t_full[slot], 0);
+                mbar_arrive_rel_cluster(&t_full[slot], 1);
+            };
+            auto fetch = [&]() {
+                const int u = atomicAdd(tile_counter, 1);
+                return u < total ? u : -1;
+            };
+            int u_next = 0;
+            if (rank == 0) {
+                u_next = fetch();
+                publish(0, u_next);
+            }
+            int g = 0;
+            for (int k = 0;; ++k) {
+                int u;
+                if (rank == 0) {
+                    u = u_next;
+                    if (u < 0) break;
+                    u_next = fetch();
+                    publish(k + 1, u_next);
+                } else {
+                    u = pair_next_tile(tinfo, t_full, t_empty, k, false);
+                    if (u < 0) break;
+                }
                 const int head = u / npq, qt = 2 * (u % npq) + static_cast<int>(rank);
                 const int seq_row0 = head * p.seq_len;
                 // Q buffer k&1 was last read by the score MMAs of tile k-2
@@ -266,8 +344,9 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             constexpr uint32_t ID_S = idesc_f16_f32(256, L::SW, 0, 0);
             const uint64_t dq = smem_desc_sw128(q_smem, 16, 1024);
             const uint64_t dk0 = smem_desc_sw128(k_smem, 16, 1024);
-            int g = 0, k = 0;
-            for (int u = cid; u < total; u += ncl, ++k) {
+            int g = 0;
+            for (int k = 0;; ++k) {
+                if (pair_next_tile(tinfo, t_full, t_empty, k, true) < 0) break;
                 const int qb = k & 1;
                 mbar_wait(qb ? q_full2 : q_full, (k >> 1) & 1);
                 tc_fence_after();
@@ -305,8 +384,9 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             constexpr uint32_t ID_PV = idesc_f16_f32(256, L::VROWS, 0, 0);
             const uint64_t dv0 = smem_desc_sw128(v_smem, 16, 1024);
             const uint32_t d_o = tmem + L::COL_O;
-            int g = 0, k = 0;
-            for (int u = cid; u < total; u += ncl, ++k) {
+            int g = 0;
+            for (int k = 0;; ++k) {
+                if (pair_next_tile(tinfo, t_full, t_empty, k, true) < 0) break;
                 for (int j = 0; j < n; ++j, ++g) {
                     EFTA_TS(10, j);
                     mbar_wait(&p_ready[g & 1], (g >> 1) & 1);
@@ -338,8 +418,8 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     } else {
         setmaxnreg_inc<232>();
         row_alt<D, PROT>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH), s_full, s_free,
-                         p_ready, o_done, o_final, mx_early, mx_late, fin_bar, o_free, tmem, warp, lane, n, cid,
-                         ncl, rank);
+                         p_ready, o_done, o_final, mx_early, mx_late, fin_bar, o_free, tmem, warp, lane, n,
+                         tinfo, t_full, t_empty, rank);
     }
 
     tc_fence_before();

@@ -263,6 +263,8 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     p.kc = reinterpret_cast<const __half*>(kc);
     const bool dbg = d->debug != 0;
     cudaError_t e;
+    if (pair)  // the persistent pair kernel's in-order tile counter (workspace scratch, int)
+        CUDA_TRY(cudaMemsetAsync(wsb + wl.scratch, 0, 16, st));
     if (pair)  // maps: q, K half A, K half B (protected peer), KC, [V^T ; VC^T]
         e = (D == 64) ? efta_launch_attn_pair_d64(d->mode, tq, tk, tv, tkc, tvc, p, bh, st)
                       : efta_launch_attn_pair_d128(d->mode, tq, tk, tv, tkc, tvc, p, bh, st);

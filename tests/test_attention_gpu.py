@@ -53,3 +53,45 @@ def test_protected_bit_identical_to_unprotected(d, seq):
     # P is rounded to fp16 relative to a different max under lazy vs eager rescaling
     assert np.abs(o2.cpu().numpy() - a0).max() <= 2e-3 * np.abs(a0).max()
     assert r1.detections == 0 and r2.detections == 0
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_persistent_pair_many_tiles(d):
+    """The production pair kernel is persistent: each cluster loops over (head, query-pair)
+    tiles with every pipeline phase carried across tiles. 512 tiles on <= 74 clusters (each
+    cluster runs ~7 tiles): parity with the CPU oracle on the first and last head, with the
+    single-CTA kernel (EFTA_NO_PAIR) on all heads, and protected == unprotected bit for bit."""
+    import os
+    import torch
+    from paper_2504_02211_b200 import EftaAttention, Thresholds
+    heads, seq = 64, 2048
+    q, k, v, _ = head_inputs(4321 + d, heads, seq, d)
+    qd, kd, vd = (_dev(x)[None] for x in (q, k, v))
+    thr = Thresholds(1e-4, 1e-3, 1e-3)
+
+    def run(mode, pair):
+        old = os.environ.pop("EFTA_NO_PAIR", None)
+        if not pair:
+            os.environ["EFTA_NO_PAIR"] = "1"
+        try:
+            op = EftaAttention(1, heads, seq, d, mode=mode, thr=thr)
+            o, m, l = op(qd, kd, vd)
+            torch.cuda.synchronize()
+            return o.cpu().numpy()[0], m.cpu().numpy()[0], l.cpu().numpy()[0], op.report()
+        finally:
+            os.environ.pop("EFTA_NO_PAIR", None)
+            if old is not None:
+                os.environ["EFTA_NO_PAIR"] = old
+
+    o_p, m_p, l_p, r_p = run("efta-opt", True)
+    o_n, _, _, _ = run("none", True)
+    o_s, m_s, l_s, r_s = run("efta-opt", False)
+    assert r_p.detections == 0 and not r_p.failed and r_s.detections == 0
+    assert np.array_equal(o_p.view(np.uint32), o_n.view(np.uint32))
+    assert np.abs(o_p - o_s).max() <= 2e-3 * np.abs(o_s).max()
+    assert np.array_equal(m_p, m_s)
+    assert np.allclose(l_p, l_s, rtol=1e-4)
+    orc = oracle()
+    for h in (0, heads - 1):
+        ref = orc.efta_forward(q[h], k[h], v[h], 128, 8, mode="none")
+        assert rel_err(o_p[h], ref.o) <= TOL, (h, rel_err(o_p[h], ref.o))
