@@ -57,7 +57,10 @@ int efta_attn_validate(const efta_attn_desc* d);
 size_t efta_attn_workspace_bytes(const efta_attn_desc* d);
 
 /* counters: device efta_counters (zeroed by the call). events/fired: device arrays
- * of the given capacities (may be NULL with cap 0). faults: device array. */
+ * of the given capacities (may be NULL with cap 0). faults: device array.
+ * workspace: device buffer of efta_attn_workspace_bytes(d) bytes (checksum operands, the
+ * persistent kernel's tile counter); calls that may run concurrently (different streams)
+ * need distinct workspaces. */
 int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t* k,
                       const uint16_t* v, float* o, float* m_out, float* l_out, void* workspace,
                       size_t workspace_bytes, const efta_fault_spec* faults, int n_faults,
