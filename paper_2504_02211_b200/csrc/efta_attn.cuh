@@ -60,7 +60,7 @@ struct AttnParams {
     int observe_linear;
     // exp-stage bracket: |ln(prod/pc1)| > eps1  <=>  prod outside [pc1*exp_lo, pc1*exp_hi]
     float exp_lo, exp_hi;
-    float* scratch;  // per-SM rows for the split schedule's rare paths (kScratchSMs x 128 x 128)
+    float* scratch;  // workspace scratch: the persistent pair kernel's tile counter (int at [0])
     unsigned long long* prof;  // EFTA_PROF builds only: phase timestamps of one CTA
     const __half* q;           // [BH, S, D]: the pair kernel's rare path recomputes score c2 from Q . KC2
     const __half* kc;          // [BH*n, 32, D] checksum rows (workspace)
@@ -86,15 +86,10 @@ struct AttnParams {
 #define EFTA_TSQ(base, j) do { } while (0)
 #endif
 
-constexpr int kScratchSMs = 256;
 
-// threads per CTA: the fast NONE / EFTA_OPT variants use the split-row schedule
-// (two row warpgroups), the tap / per-iteration-check variants one row warpgroup
-__host__ __device__ constexpr bool attn_split(int mode, bool dbg) { return false && !dbg && mode != 1; }
 // fast variants rescale O lazily (only when the running max grows by > kLazyTau)
 __host__ __device__ constexpr bool attn_lazy(int mode, bool dbg) { return !dbg && mode != 1; }
 constexpr float kLazyTau = 5.545177444479562f;  // 8 * ln 2: P <= 2^8 between rescales
-__host__ __device__ constexpr int attn_threads(int mode, bool dbg) { return attn_split(mode, dbg) ? 384 : 256; }
 
 template <int D>
 struct AttnLayout {
@@ -123,10 +118,7 @@ struct AttnLayout {
     static constexpr uint32_t OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
     static constexpr uint32_t RED_BYTES = 128 * 24 + 256;  // RowSlot[128] + ints + doubles
-    // split-row exchange area: xmax[2][2][128], xprod[128][16], xpub[128][4], xl[2][128] floats
-    static constexpr uint32_t OFF_XCH = OFF_RED + RED_BYTES;
-    static constexpr uint32_t XCH_BYTES = (512 + 2048 + 512 + 256) * 4;
-    static constexpr uint32_t SMEM_BYTES = OFF_XCH + XCH_BYTES + 1024;  // + alignment slack
+    static constexpr uint32_t SMEM_BYTES = OFF_RED + RED_BYTES + 1024;  // + alignment slack
     // TMEM: S[b] = b*160: cols 0..127 scores (P aliased over 0..63), 128..143 checksum
     // hi-products, 144..159 lo-products; O at 320: D cols + 16 hi + 16 lo checksum cols.
     static constexpr uint32_t S_STRIDE = 160;

@@ -27,7 +27,7 @@ cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtenso
         attr_set = true;
     }
     dim3 grid(p.nblk, bh);
-    kern<<<grid, attn_threads(MODE, DBG), L::SMEM_BYTES, st>>>(tq, tk, tv, tkc, tvc, p);
+    kern<<<grid, 256, L::SMEM_BYTES, st>>>(tq, tk, tv, tkc, tvc, p);
     return cudaGetLastError();
 }
 

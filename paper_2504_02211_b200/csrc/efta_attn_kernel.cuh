@@ -316,11 +316,6 @@ __device__ __forceinline__ void verify_output_tile(const AttnParams& p, float (&
                    tr.corrections, tr.checksum_repair, tr.residual, tr.delta);
 }
 
-}  // namespace efta_sm100
-
-#include "efta_attn_split.cuh"
-
-namespace efta_sm100 {
 
 
 template <bool PAIR>
@@ -813,13 +808,12 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
 
 // ----------------------------------------------------------------------------
 template <int D, int MODE, bool DBG>
-__global__ void __launch_bounds__(attn_threads(MODE, DBG), 1)
+__global__ void __launch_bounds__(256, 1)
 efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
                      const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
     using L = AttnLayout<D>;
     constexpr bool PROT = MODE != EFTA_MODE_NONE;
-    constexpr bool SPLIT = attn_split(MODE, DBG);
     constexpr bool LAZY = attn_lazy(MODE, DBG);
     constexpr int KS = L::KS, VS = L::VS, NSUB = L::NSUB;
 
@@ -846,7 +840,7 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
         for (int s = 0; s < VS; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
         mbar_init(&s_full[0], 1);
         mbar_init(&s_full[1], 1);
-        mbar_init(p_ready, SPLIT ? 256 : 128);
+        mbar_init(p_ready, 128);
         mbar_init(o_done, 1);
         fence_barrier_init();
         tma_prefetch_desc(&tm_q);
@@ -952,14 +946,7 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
             }
         }
         __syncwarp();
-    } else if (SPLIT && warp >= 4) {
-        RowScratch rs2;
-        rs2.slots = reinterpret_cast<RowSlot*>(smem + L::OFF_RED);
-        rs2.ints = reinterpret_cast<int*>(smem + L::OFF_RED + 128 * sizeof(RowSlot));
-        rs2.dbl = reinterpret_cast<double*>(smem + L::OFF_RED + 128 * sizeof(RowSlot) + 16 * sizeof(int));
-        row_split<D, PROT>(p, s_full, p_ready, o_done, tmem, warp, lane, head, qt, n, seq_row0, rs2,
-                           reinterpret_cast<float*>(smem + L::OFF_XCH));
-    } else if (!SPLIT && warp >= 4) {
+    } else if (warp >= 4) {
         row_wg<D, MODE, DBG, false>(p, smem + L::OFF_RED, s_full, p_ready, o_done, tmem, warp, lane, head, qt, n, seq_row0);
     }
     tc_fence_before();

@@ -91,7 +91,7 @@ int validate(const efta_attn_desc* d) {
 }
 
 // Workspace: [KC: bh*n*32*d fp16] [R2: max(single-CTA VC bh*n*128*64, pair V^T+VC^T
-// bh*n*(d+32)*128) fp16] [per-SM scratch rows]. All offsets 256-byte aligned.
+// bh*n*(d+32)*128) fp16] [scratch: 256 B, the persistent pair kernel tile counter]. All offsets 256-byte aligned.
 struct WsLayout {
     size_t kc, r2, scratch, total;
 };
@@ -104,7 +104,7 @@ WsLayout ws_layout(const efta_attn_desc* d) {
     w.r2 = al(bh * nblk * 32 * d->head_dim * sizeof(__half));
     const size_t r2 = std::max(bh * nblk * 128 * 64, bh * nblk * (d->head_dim + 32) * 128) * sizeof(__half);
     w.scratch = w.r2 + al(r2);
-    w.total = w.scratch + static_cast<size_t>(kScratchSMs) * 128 * 128 * sizeof(float);
+    w.total = w.scratch + 256;  // scratch: the persistent pair kernel's tile counter
     return w;
 }
 size_t ws_bytes(const efta_attn_desc* d) { return ws_layout(d).total; }
