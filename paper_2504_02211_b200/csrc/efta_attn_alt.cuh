@@ -166,14 +166,10 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                 pv[c + 1] = e.y;
                 if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
                 else ps0 = fadd2(ps0, e);
-#ifndef EFTA_ABL_NOPROD
                 if (PROT) {
                     const int g = (c & 7) >> 1;
                     prod_f[g] = (c < kStride) ? e : fmul2(prod_f[g], e);
                 }
-#else
-                if (PROT && c < kStride) prod_f[(c & 7) >> 1] = e;
-#endif
             }
             psum_f = (ps0.x + ps0.y) + (ps1.x + ps1.y);
             if (!PROT) break;  // no recovery path: the chain can never be revised
@@ -190,30 +186,20 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                 if (bad) { exp_affected = true; ++exp_viol; }
             }
             float exp_res = 0.0f;
-#ifdef EFTA_ABL_NOPROD  // timing ablation only: no exp-stage check
-            exp_affected = false;
-            exp_viol = 0;
-#endif
             if (degenerate) { exp_affected = true; exp_res = CUDART_INF_F; exp_viol = 1; }
             const bool factor_bad = (j > 0) && !(f > 0.0f && f <= 1.0f);
             // ---- late chain check: did the partner's decision revise block j-1's maxima?
             bool chain_bad = false;
             if (j > 0) {
                 if ((warp & 3) == 0) EFTA_TS(8, j);
-#ifndef EFTA_ABL_NOLATE
                 if (attempt == 0) mbar_wait(pa_late, pph);
-#endif
                 const float2 c = xc->late[1 - w][row];
                 chain_bad = __float_as_uint(c.x) != __float_as_uint(m_true_prev) ||
                             __float_as_uint(c.y) != __float_as_uint(m_run_prev);
             }
             if ((warp & 3) == 0) EFTA_TS(9, j);
             EFTA_TSQ(0, j);
-#ifdef EFTA_ABL_NOBAR  // timing ablation only: no tile-wide decision
-            if (!__any_sync(0xffffffffu, exp_affected || factor_bad || chain_bad)) break;
-#else
             if (!named_bar_or(6 + bo, 128, exp_affected || factor_bad || chain_bad)) break;
-#endif
             if (named_bar_or(6 + bo, 128, chain_bad)) continue;  // redo the block with the revised maxima
             // ---- rare: the reference recovery ladder for this tile
             float p_loc[kBlock];
