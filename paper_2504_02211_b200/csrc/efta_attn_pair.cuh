@@ -432,6 +432,8 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
 // Prepass for the pair kernel: KC (as before) + [V_j^T ; VC_j^T] per (head, block):
 //   VT[(head*n + j) * VROWS + r][key] = V[j*128 + key][r]                         r < D
 //   VT[(head*n + j) * VROWS + D + x / 8+x / 16+x / 24+x][key] = c1_hi / c2_hi / c1_lo / c2_lo
+// HBM-bound: every global access is a 16-byte vector (8 halves), V is transposed through
+// shared memory, the strided sums run in fp32 in ascending l / g (the reference order).
 template <int D, bool PROT>
 __global__ void __launch_bounds__(256) efta_encode_pair_kernel(const __half* __restrict__ k,
                                                                const __half* __restrict__ v,
@@ -439,52 +441,84 @@ __global__ void __launch_bounds__(256) efta_encode_pair_kernel(const __half* __r
                                                                int seq_len, int nblk) {
     constexpr int VROWS = PROT ? D + 32 : D;
     constexpr int G_O = D / 8;
-    __shared__ __half sv[128 * (D + 8)];
+    // V block in shared memory, row `key` at key*SP + (key/8)*8 halves: 16-byte aligned rows, and
+    // the column reads of the transpose (keys 8 apart across a warp) spread over 8 banks
+    constexpr int SP = D + 8;
+    __shared__ __align__(16) __half sv[128 * SP + 16 * 8];
+    auto sidx = [](int key, int c) { return key * SP + (key >> 3) * 8 + c; };
     const int j = blockIdx.x, head = blockIdx.y;
     const size_t row0 = static_cast<size_t>(head) * seq_len + static_cast<size_t>(j) * 128;
     for (int idx = threadIdx.x; idx < 128 * D / 8; idx += blockDim.x) {
         const int r = idx / (D / 8), c8 = idx % (D / 8);
-        *reinterpret_cast<uint4*>(&sv[r * (D + 8) + c8 * 8]) = reinterpret_cast<const uint4*>(v + (row0 + r) * D)[c8];
+        *reinterpret_cast<uint4*>(&sv[sidx(r, c8 * 8)]) = reinterpret_cast<const uint4*>(v + (row0 + r) * D)[c8];
     }
     if (PROT) {
+        // KC rows: thread = (group x, 8 consecutive dims); 16 vector loads of K rows x + 8l
         const size_t crow0 = (static_cast<size_t>(head) * nblk + j) * 32;
-        for (int t = threadIdx.x; t < 8 * D; t += blockDim.x) {
-            const int x = t / D, dim = t % D;
-            float c1 = 0.0f, c2 = 0.0f;
+        for (int t = threadIdx.x; t < 8 * (D / 8); t += blockDim.x) {
+            const int x = t / (D / 8), d8 = t % (D / 8);
+            float c1[8], c2[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { c1[i] = 0.0f; c2[i] = 0.0f; }
 #pragma unroll
             for (int l = 0; l < 16; ++l) {
-                const float val = __half2float(k[(row0 + x + 8 * l) * D + dim]);
-                c1 = __fadd_rn(c1, val);
-                c2 = __fadd_rn(c2, __fmul_rn(static_cast<float>(l + 1), val));
+                const uint4 raw = reinterpret_cast<const uint4*>(k + (row0 + x + 8 * l) * D)[d8];
+                const __half* hv = reinterpret_cast<const __half*>(&raw);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float val = __half2float(hv[i]);
+                    c1[i] = __fadd_rn(c1[i], val);
+                    c2[i] = __fadd_rn(c2[i], __fmul_rn(static_cast<float>(l + 1), val));
+                }
             }
-            const __half h1 = __float2half_rn(c1), h2 = __float2half_rn(c2);
-            kc[(crow0 + x) * D + dim] = h1;
-            kc[(crow0 + 8 + x) * D + dim] = h2;
-            kc[(crow0 + 16 + x) * D + dim] = __float2half_rn(__fsub_rn(c1, __half2float(h1)));
-            kc[(crow0 + 24 + x) * D + dim] = __float2half_rn(__fsub_rn(c2, __half2float(h2)));
+            __align__(16) __half h1[8], h2[8], l1[8], l2[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                h1[i] = __float2half_rn(c1[i]);
+                h2[i] = __float2half_rn(c2[i]);
+                l1[i] = __float2half_rn(__fsub_rn(c1[i], __half2float(h1[i])));
+                l2[i] = __float2half_rn(__fsub_rn(c2[i], __half2float(h2[i])));
+            }
+            reinterpret_cast<uint4*>(kc + (crow0 + x) * D)[d8] = *reinterpret_cast<const uint4*>(h1);
+            reinterpret_cast<uint4*>(kc + (crow0 + 8 + x) * D)[d8] = *reinterpret_cast<const uint4*>(h2);
+            reinterpret_cast<uint4*>(kc + (crow0 + 16 + x) * D)[d8] = *reinterpret_cast<const uint4*>(l1);
+            reinterpret_cast<uint4*>(kc + (crow0 + 24 + x) * D)[d8] = *reinterpret_cast<const uint4*>(l2);
         }
     }
     __syncthreads();
     __half* dst = vt + (static_cast<size_t>(head) * nblk + j) * VROWS * 128;
-    for (int t = threadIdx.x; t < D * 128; t += blockDim.x) {  // transpose: coalesced over keys
-        const int r = t / 128, key = t % 128;
-        dst[r * 128 + key] = sv[key * (D + 8) + r];
+    // transpose: thread = (dim r, 8 consecutive keys) -> one 16-byte store
+    for (int t = threadIdx.x; t < D * 16; t += blockDim.x) {
+        const int r = t / 16, k8 = t % 16;
+        __align__(16) __half h[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) h[i] = sv[sidx(k8 * 8 + i, r)];
+        reinterpret_cast<uint4*>(dst + r * 128)[k8] = *reinterpret_cast<const uint4*>(h);
     }
     if (PROT) {
-        for (int t = threadIdx.x; t < 8 * 128; t += blockDim.x) {
-            const int x = t / 128, key = t % 128;
-            float c1 = 0.0f, c2 = 0.0f;
+        // VC rows: thread = (group x, 8 consecutive keys)
+        for (int t = threadIdx.x; t < 8 * 16; t += blockDim.x) {
+            const int x = t / 16, k8 = t % 16;
+            __align__(16) __half h1[8], h2[8], l1[8], l2[8];
 #pragma unroll
-            for (int g = 0; g < G_O; ++g) {
-                const float val = __half2float(sv[key * (D + 8) + x + 8 * g]);
-                c1 = __fadd_rn(c1, val);
-                c2 = __fadd_rn(c2, __fmul_rn(static_cast<float>(g + 1), val));
+            for (int i = 0; i < 8; ++i) {
+                const int key = k8 * 8 + i;
+                float c1 = 0.0f, c2 = 0.0f;
+#pragma unroll
+                for (int g = 0; g < G_O; ++g) {
+                    const float val = __half2float(sv[sidx(key, x + 8 * g)]);
+                    c1 = __fadd_rn(c1, val);
+                    c2 = __fadd_rn(c2, __fmul_rn(static_cast<float>(g + 1), val));
+                }
+                h1[i] = __float2half_rn(c1);
+                h2[i] = __float2half_rn(c2);
+                l1[i] = __float2half_rn(__fsub_rn(c1, __half2float(h1[i])));
+                l2[i] = __float2half_rn(__fsub_rn(c2, __half2float(h2[i])));
             }
-            const __half h1 = __float2half_rn(c1), h2 = __float2half_rn(c2);
-            dst[(D + x) * 128 + key] = h1;
-            dst[(D + 8 + x) * 128 + key] = h2;
-            dst[(D + 16 + x) * 128 + key] = __float2half_rn(__fsub_rn(c1, __half2float(h1)));
-            dst[(D + 24 + x) * 128 + key] = __float2half_rn(__fsub_rn(c2, __half2float(h2)));
+            reinterpret_cast<uint4*>(dst + (D + x) * 128)[k8] = *reinterpret_cast<const uint4*>(h1);
+            reinterpret_cast<uint4*>(dst + (D + 8 + x) * 128)[k8] = *reinterpret_cast<const uint4*>(h2);
+            reinterpret_cast<uint4*>(dst + (D + 16 + x) * 128)[k8] = *reinterpret_cast<const uint4*>(l1);
+            reinterpret_cast<uint4*>(dst + (D + 24 + x) * 128)[k8] = *reinterpret_cast<const uint4*>(l2);
         }
     }
 }
