@@ -45,7 +45,7 @@ constexpr uint32_t OFF_BAR = STAGES * STAGE;
 constexpr uint32_t OFF_TMEM = OFF_BAR + (2 * STAGES + 2) * 8;
 constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
 constexpr uint32_t OFF_XS = OFF_RED + 128 * 24 + 256;  // column half 1's partial strided sums [128][16]
-constexpr uint32_t SMEM_BYTES = OFF_XS + 128 * 16 * 4 + 1024;
+constexpr uint32_t SMEM_BYTES = OFF_XS + 128 * 16 * 4 + 16 + 1024;
 constexpr int GEMM_THREADS = 384;  // warps 0-3: TMA / MMA / idle / idle; 4-11: epilogue (2 column halves)
 
 struct GemmParams {
@@ -155,6 +155,7 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
         rs.ints = reinterpret_cast<int*>(smem + OFF_RED + 128 * sizeof(RowSlot));
         rs.dbl = reinterpret_cast<double*>(smem + OFF_RED + 128 * sizeof(RowSlot) + 16 * sizeof(int));
         float* xs = reinterpret_cast<float*>(smem + OFF_XS) + row * 16;
+        int* dec = reinterpret_cast<int*>(smem + OFF_XS + 128 * 16 * 4);  // the lower half's tile verdict
         float fam = 0.0f;
         int tl = 0;
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
@@ -174,44 +175,62 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
 #pragma unroll
             for (int x = 0; x < 8; ++x) { s1[x] = 0.0f; s2[x] = 0.0f; }
             __half* yrow = p.y + static_cast<size_t>(grow) * p.n + nt * GN;
-            bool nonfin = false;
-#pragma unroll 1
-            for (int c = half * 4; c < half * 4 + 4; ++c) {
-                float v[32];
-                tmem_ld32(lb + (c < 4 ? c * 32 : 144 + (c - 4) * 32), *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-                tmem_wait_ld();
-                if (DBG && f_col >= c * 32 && f_col < c * 32 + 32) {
+            // this half's 128 accumulator columns into registers (one wait for all four loads)
+            float v[128];
 #pragma unroll
-                    for (int x = 0; x < 32; ++x)
-                        if (x == f_col - c * 32) v[x] = __uint_as_float(__float_as_uint(v[x]) ^ (1u << f_bit));
-                }
-#pragma unroll
-                for (int l4 = 0; l4 < 4; ++l4) {
-                    const float w = static_cast<float>(c * 4 + l4 + 1);
-#pragma unroll
-                    for (int x = 0; x < 8; ++x) {
-                        const float val = v[l4 * 8 + x];
-                        s1[x] = __fadd_rn(s1[x], val);
-                        s2[x] = __fadd_rn(s2[x], __fmul_rn(w, val));
-                        nonfin |= !isfinite(val);
-                    }
-                }
-                uint4 pk[4];
-                uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-                for (int x = 0; x < 16; ++x) pw[x] = pack_half2(v[2 * x], v[2 * x + 1]);
-                uint4* dst = reinterpret_cast<uint4*>(yrow + c * 32);
-#pragma unroll
-                for (int x = 0; x < 4; ++x) dst[x] = pk[x];
+            for (int c4 = 0; c4 < 4; ++c4) {
+                const int c = half * 4 + c4;
+                tmem_ld32(lb + (c < 4 ? c * 32 : 144 + (c - 4) * 32), *reinterpret_cast<uint32_t(*)[32]>(&v[c4 * 32]));
             }
+            tmem_wait_ld();
+            if (DBG && f_col >= half * 128 && f_col < half * 128 + 128) {
+#pragma unroll
+                for (int x = 0; x < 128; ++x)
+                    if (x == f_col - half * 128) v[x] = __uint_as_float(__float_as_uint(v[x]) ^ (1u << f_bit));
+            }
+            bool nonfin = false;
+#pragma unroll
+            for (int l = 0; l < 16; ++l) {
+                const float w = static_cast<float>(half * 16 + l + 1);
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    const float val = v[l * 8 + x];
+                    s1[x] = __fadd_rn(s1[x], val);
+                    s2[x] = __fadd_rn(s2[x], __fmul_rn(w, val));
+                    nonfin |= !isfinite(val);
+                }
+            }
+            // fp16 output of this half: packed and stored once the accumulator is released
+            auto store_half = [&]() {
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    uint4 pk[4];
+                    uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) pw[x] = pack_half2(v[c4 * 32 + 2 * x], v[c4 * 32 + 2 * x + 1]);
+                    uint4* dst = reinterpret_cast<uint4*>(yrow + (half * 4 + c4) * 32);
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) dst[x] = pk[x];
+                }
+            };
             if (half == 1) {
-                // hand the partial sums of groups l = 16..31 to the lower half; its verdict
-                // (and any correction) follows from the still-resident accumulator
+                // hand the partial sums of groups l = 16..31 to the lower half, wait for its
+                // verdict; a clean tile releases the accumulator before the stores
 #pragma unroll
                 for (int x = 0; x < 8; ++x) { xs[x] = s1[x]; xs[8 + x] = s2[x]; }
                 named_bar_arrive(6, 256);
-                tc_fence_before();
-                mbar_arrive(tempty);
+                named_bar_sync(7, 256);
+                const bool rare = *reinterpret_cast<volatile int*>(dec) != 0;
+                if (!rare) {
+                    tc_fence_before();
+                    mbar_arrive(tempty);
+                }
+                store_half();
+                if (rare) {
+                    named_bar_arrive(8, 256);  // raw values stored before the lower half corrects
+                    tc_fence_before();
+                    mbar_arrive(tempty);
+                }
                 continue;
             }
             named_bar_sync(6, 256);
@@ -240,7 +259,18 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
             }
             fam = fmaxf(fam, static_cast<float>(res));
             const bool tile_cs_bad = named_bar_or(4, 128, cs_bad);
-            if (named_bar_or(5, 128, viol || cs_bad)) {
+            const bool any = named_bar_or(5, 128, viol || cs_bad);
+            if (row == 0) *dec = any ? 1 : 0;
+            named_bar_arrive(7, 256);
+            if (!any) {
+                tc_fence_before();
+                mbar_arrive(tempty);
+                store_half();
+                continue;
+            }
+            store_half();
+            named_bar_sync(8, 256);  // the upper half's raw values are stored too
+            {
                 // locate / correct from the still-resident accumulator row
                 RowVerify rv{};
                 rv.best_col = -1;
