@@ -286,7 +286,7 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
     // (separate copy engines; PCIe is full duplex). Fault-injection calls (head-indexed
     // fault tables, fired lists) run as one chunk.
     const int bh = d->batch * d->heads;
-    const int nchunk = (n_faults > 0 || fired) ? 1 : std::min(bh, 8);
+    const int nchunk = (n_faults > 0 || fired) ? 1 : std::min(bh, 32);  // small first-H2D / last-D2H tails
     const int per = (bh + nchunk - 1) / nchunk;
     struct Scratch {
         void* p = nullptr;
