@@ -117,11 +117,12 @@ def run_gpu_campaign(n_trials=20, heads=12, seq_len=512, head_dim=64, sites=None
         thr, _ = calibrate_thresholds(seq_len, head_dim, mode, calibrate_trials, 2.0,
                                       seed ^ 0xCA11B7A7, device)
     n_rec = n_trials * heads
-    qs, ks, vs, specs = [], [], [], []
+    qs, ks, vs, specs, seeds = [], [], [], [], []
     for t in range(n_trials):
         tseed = trial_seed(seed, t)
         for h in range(heads):
             hseed = tseed if heads == 1 else trial_seed(tseed, h)
+            seeds.append(hseed)
             q, k, v, f = gen_head(hseed, seq_len, head_dim, sites=None if fixed_plan else sites)
             if fixed_plan is not None:
                 f = FaultSpec.parse(fixed_plan) if isinstance(fixed_plan, str) else fixed_plan
@@ -150,12 +151,24 @@ def run_gpu_campaign(n_trials=20, heads=12, seq_len=512, head_dim=64, sites=None
     l_np = l.view(n_rec, seq_len).cpu().numpy()
     records = []
     stats = {k2: 0 for k2 in OUTCOMES}
+    corr = [0] * n_rec
+    reco = [0] * n_rec
+    for e in rep.events:
+        corr[e["head"]] += e["corrections"]
+        if e["kind"] in ("exp_checksum", "factor_range") and e["status"] == "corrected":
+            reco[e["head"]] += 1
     for i in range(n_rec):
         out = classify(o_np[i], r_np[i], det[i], rr[i], failed[i], l_np[i], specs[i], thr.eps2)
         stats[out] += 1
-        records.append(dict(trial=i // heads, head=i % heads, fault=specs[i].to_string(),
-                            fired=i in fired_heads, detections=det[i], outcome=out,
-                            residual_out=float(np.abs(o_np[i].astype(np.float64) - r_np[i]).max())))
+        res = float(np.abs(o_np[i].astype(np.float64) - r_np[i]).max())
+        ref_inf = float(np.abs(r_np[i]).max())
+        records.append(dict(trial=i // heads, head=i % heads, seed=seeds[i], injected=True,
+                            fired=i in fired_heads, fault=specs[i].to_string(),
+                            site=SITES[specs[i].site], bit=specs[i].bit, detections=det[i],
+                            corrections=corr[i], recomputes=reco[i], range_replacements=rr[i],
+                            failed=failed[i], argmax_ok=rows_argmax_match(o_np[i], r_np[i]),
+                            residual_out=res, rel_residual_out=res / ref_inf if ref_inf > 0 else 0.0,
+                            outcome=out))
     n_fired = sum(r["fired"] for r in records)
     bad = sum(1 for r in records if r["fired"] and r["outcome"] == "uncorrectable")
     return {"records": n_rec, "fired": n_fired, "coverage": 1.0 - bad / n_fired if n_fired else 1.0,
@@ -164,3 +177,72 @@ def run_gpu_campaign(n_trials=20, heads=12, seq_len=512, head_dim=64, sites=None
             "range_contract": stats["range_contract"], "uncorrectable": stats["uncorrectable"],
             "false_alarms": rep_clean.detections, "thresholds": (thr.eps1, thr.eps2, thr.eps_lin),
             "detail": records, "events": rep.events}
+
+
+# ---------------------------------------------------------------- wire formats
+# trials.csv (src/campaign.cpp:359-372) and summary.json (tools/efta_main.cpp:117-162) written
+# from GPU campaign records. Doubles follow C++ ostream defaults (6 significant digits).
+TRIALS_CSV_HEADER = ("trial,head,seed,injected,fired,site,bit,fault,detections,corrections,recomputes,"
+                     "range_replacements,failed,argmax_ok,residual_out,rel_residual_out,outcome")
+
+
+def rows_argmax_match(a: np.ndarray, b: np.ndarray) -> bool:
+    """rows_argmax_match (src/campaign.cpp:25-36) behind the finite guard of :130."""
+    if a.shape != b.shape or not np.isfinite(a).all():
+        return False
+    return bool(np.array_equal(np.argmax(a, axis=1), np.argmax(b, axis=1)))
+
+
+def _g(x: float) -> str:
+    return f"{x:.6g}"
+
+
+def write_trials_csv(path: str, records) -> None:
+    with open(path, "w") as f:
+        f.write(TRIALS_CSV_HEADER + "\n")
+        for r in records:
+            f.write(",".join([str(r["trial"]), str(r["head"]), str(r["seed"]), str(int(r["injected"])),
+                              str(int(r["fired"])), r["site"], str(r["bit"]), r["fault"],
+                              str(r["detections"]), str(r["corrections"]), str(r["recomputes"]),
+                              str(r["range_replacements"]), str(int(r["failed"])), str(int(r["argmax_ok"])),
+                              _g(r["residual_out"]), _g(r["rel_residual_out"]), r["outcome"]]) + "\n")
+
+
+def campaign_stats(records) -> dict:
+    """CampaignStats aggregation (src/campaign.cpp:236-256) + coverage (:103-111)."""
+    st = dict(trials=0, injected=0, fired=0, detected=0, false_alarms=0, corrected=0, range_restricted=0,
+              masked_benign=0, range_contract=0, uncorrectable=0, argmax_preserved=0,
+              max_corrected_residual=0.0)
+    for r in records:
+        st["trials"] += 1
+        st["injected"] += int(r["injected"])
+        st["fired"] += int(r["fired"])
+        st["detected"] += int(r["detections"] > 0)
+        st["argmax_preserved"] += int(r["injected"] and r["argmax_ok"])
+        o = r["outcome"]
+        if o == "false_alarm":
+            st["false_alarms"] += 1
+        elif o != "clean":
+            st[o] += 1
+        if o == "corrected":
+            st["max_corrected_residual"] = max(st["max_corrected_residual"], r["residual_out"])
+    st["coverage"] = 1.0 - st["uncorrectable"] / st["fired"] if st["fired"] else 1.0
+    return st
+
+
+def write_summary_json(path: str, records, mode: str, seq_len: int, head_dim: int, heads: int,
+                       thr: Thresholds, block: int = 128, stride: int = 8, scale: float | None = None,
+                       calibration: dict | None = None) -> dict:
+    """summary.json with the reference's mode / config / thresholds / stats keys. The reference's
+    analytic `counters` and `overhead` blocks are CPU operation counts; the GPU reports measured
+    time instead (bench.py), so they are omitted."""
+    import json
+    j = {"mode": {"efta-opt": "efta-opt", "efta": "efta", "none": "none"}[mode],
+         "config": {"seq_len": seq_len, "head_dim": head_dim, "block": block, "stride": stride, "heads": heads,
+                    "scale": scale if scale is not None else 1.0 / math.sqrt(head_dim)},
+         "thresholds": {**({"calibrated": True, **calibration} if calibration else {"calibrated": False}),
+                        "eps1": thr.eps1, "eps2": thr.eps2, "eps_lin": thr.eps_lin},
+         "stats": campaign_stats(records)}
+    with open(path, "w") as f:
+        f.write(json.dumps(j, indent=2) + "\n")
+    return j
