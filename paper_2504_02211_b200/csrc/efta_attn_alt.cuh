@@ -47,6 +47,21 @@ struct AltXch {
 };
 static_assert(sizeof(AltXch) == 6144, "PairLayout reserves 6 KB for the chain exchange");
 
+// explicit shared-space loads (a generic pointer would compile to the slower generic LD path)
+__device__ __forceinline__ float2 lds_f2(const float2* p) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ float4 lds_f4(const float4* p) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(smem_u32(p))
+                 : "memory");
+    return v;
+}
+
 template <int D, bool PROT>
 __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, uint64_t* s_full,
                                         uint64_t* s_free, uint64_t* p_ready, uint64_t* o_done, uint64_t* o_final,
@@ -124,11 +139,11 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             if (j > 0) {
                 if (attempt == 0) {
                     mbar_wait(pa_early, pph);
-                    const float2 c = xc->early[1 - w][row];
+                    const float2 c = lds_f2(&xc->early[1 - w][row]);
                     m_true_prev = c.x;
                     m_run_prev = c.y;
                 } else {
-                    const float2 c = xc->late[1 - w][row];
+                    const float2 c = lds_f2(&xc->late[1 - w][row]);
                     m_true_prev = c.x;
                     m_run_prev = c.y;
                 }
@@ -193,7 +208,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             if (j > 0) {
                 if ((warp & 3) == 0) EFTA_TS(8, j);
                 if (attempt == 0) mbar_wait(pa_late, pph);
-                const float2 c = xc->late[1 - w][row];
+                const float2 c = lds_f2(&xc->late[1 - w][row]);
                 chain_bad = __float_as_uint(c.x) != __float_as_uint(m_true_prev) ||
                             __float_as_uint(c.y) != __float_as_uint(m_run_prev);
             }
@@ -299,7 +314,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         continue;
     }
     mbar_wait(&fin_bar[wq], static_cast<uint32_t>(k) & 1u);
-    const float4 fb = xc->fin[row];
+    const float4 fb = lds_f4(&xc->fin[row]);
     float m_run = m_ref;  // the chain's final reference max (block n-1 is ours)
     const float m_true = m_true_last;
     const float fbf = ex2_approx((fb.z - m_run) * kLog2e);
