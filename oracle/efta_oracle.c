@@ -903,7 +903,7 @@ int eorc_gen_trial(uint64_t seed, int n, int d, int block, int stride, const int
 int eorc_standard_attention(int n, int d, int block, int stride, float scale, const float* q,
                             const float* k, const float* v, float* o) {
     if (validate_cfg(n, d, block, stride, &scale)) return 1;
-    float* kt = (float*)malloc(sizeof(float) * (size_t)d * n);
+    float* kt = (float*)calloc((size_t)d * n, sizeof(float));
     float* s = (float*)malloc(sizeof(float) * (size_t)n * n);
     for (int r = 0; r < n; ++r)
         for (int c = 0; c < d; ++c) kt[(size_t)c * n + r] = k[(size_t)r * d + c];
