@@ -2,7 +2,7 @@
 
 * the chunked, three-stream host entry point (efta_attn_fwd_host_f16, the reference-facing
   e2e call) reproduces the device entry point bit for bit;
-* the rare recovery ladder of the CTA-pair kernel (split-row schedule, c1-only score MMA,
+* the rare recovery ladder of the CTA-pair kernel (alternating row warpgroups, c1-only score MMA,
   c2 on the CUDA cores) takes the same decisions as the single-CTA kernel when a checksum
   operand is corrupted in the workspace (a "natural" upset the tap variant cannot model).
 """
