@@ -8,7 +8,7 @@
 //
 // Here two row warpgroups own ALTERNATE key blocks of the same 128 query rows:
 // warpgroup w (warps 4+4w .. 7+4w) processes blocks j = w, w+2, ... from S buffer w
-// (the S accumulator is already double-buffered by block parity, so no extra TMEM).
+// (S is double-buffered by block parity; P has its own TMEM buffer, efta_attn_pair.cuh).
 // Each sub-partition now runs two independent softmax warps. The online-softmax
 // recurrence (src/efta.cpp:192-260) couples consecutive blocks only through the row
 // maxima; those are handed from one warpgroup to the other through shared memory:
@@ -22,22 +22,25 @@
 //     max) it recomputes its block from the still-resident S with the revised values,
 //     which reproduces the sequential recurrence exactly.
 // Row sums l and the range lower bound lb are kept per warpgroup, each referenced to
-// the warpgroup's own last reference max, and merged at the end
+// the warpgroup's own last reference max, and merged at the end of the tile
 // (l = l_0 e^{m_0 - m} + l_1 e^{m_1 - m}). O is one TMEM accumulator for both; it is
 // rescaled (lazily, kLazyTau) by the warpgroup whose block moved the reference max,
 // after P.V of the previous block completed.
 //
-// Barriers: per warpgroup a P-ready barrier (4 warps x 2 CTAs), per (warpgroup, warp
-// quarter) an early and a late chain barrier (32 arrivals). Named barriers: warpgroup 0
-// uses the single-warpgroup ids 1..7, warpgroup 1 the same + kBarAltOfs (9, 10, 11, 14),
-// id 8 hands warpgroup 1's sums to warpgroup 0, which alone runs the epilogue.
+// Persistent: the warpgroups loop over the cluster's tiles (pair_next_tile); warpgroup 1
+// runs block n-1 of a tile, receives warpgroup 0's sums through shared memory (fin_bar)
+// and runs the epilogue while warpgroup 0 already starts the next tile.
+//
+// Barriers: per warpgroup a P-ready and an S-free barrier (4 warps x 2 CTAs), per
+// (warpgroup, warp quarter) an early and a late chain barrier (32 arrivals). Named
+// barriers: warpgroup 0 uses the single-warpgroup ids 1..7, warpgroup 1 the same +
+// kBarAltOfs (9, 10, 11, 14 in the loop; 9, 12, 13, 15 in the epilogue).
 #pragma once
 #include "efta_attn_kernel.cuh"
 // included by efta_attn_pair.cuh after PairLayout
 
 namespace efta_sm100 {
 
-constexpr uint32_t kBarAltFin = 8;
 constexpr uint32_t kBarAltOfs = 8;
 
 struct AltXch {
