@@ -47,9 +47,12 @@ typedef struct {
     double eps1, eps2, eps_lin; /* reference Thresholds (snvr.hpp:17-30) */
     int observe_linear; /* KernelKnobs::observe_linear (efta.hpp:79) */
     float rowmax_bias;  /* KernelKnobs::rowmax_bias (efta.hpp:82) */
-    int debug;          /* 1: fault-tap / observation kernel variant (required if n_faults > 0) */
-    int checksums_ready;/* 1: workspace already holds this K/V's checksum operands (skip the
-                           encode prepass; e.g. K/V reused across calls) */
+    int debug;          /* 1: fault-tap / observation build (required if n_faults > 0): the
+                           reference op sequence with taps at every FaultSite, eager rescale */
+    int checksums_ready;/* 1: workspace already holds this K/V's encoded operands (skip the
+                           prepass; e.g. K/V reused across calls). On the CTA-pair path the
+                           workspace also holds the transposed V operand ([V^T ; VC^T]), so the
+                           flag covers V itself, in every mode. Ignored by the host path. */
 } efta_attn_desc;
 
 const char* efta_last_error(void);

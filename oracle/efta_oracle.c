@@ -72,6 +72,12 @@ static uint32_t rng_below(rng_t* r, uint32_t n) {
     }
 }
 
+void eorc_rng_below_seq(uint64_t seed, int n, const uint32_t* bounds, uint32_t* out) {
+    rng_t r;
+    rng_init(&r, seed);
+    for (int i = 0; i < n; ++i) out[i] = rng_below(&r, bounds[i]);
+}
+
 /* rng.hpp:8-13 */
 static uint64_t splitmix64(uint64_t* state) {
     uint64_t z = (*state += 0x9e3779b97f4a7c15ull);

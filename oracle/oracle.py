@@ -117,6 +117,8 @@ class Oracle:
         self._random_matrix = fn("random_matrix")
         self._random_matrix.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_double, C.c_double,
                                         C.c_int, _f32p]
+        self._below = fn("rng_below_seq")
+        self._below.argtypes = [C.c_uint64, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         self._flip = fn("flip_bit")
         self._flip.restype = C.c_float
         self._flip.argtypes = [C.c_float, C.c_int, C.c_int]
@@ -168,6 +170,14 @@ class Oracle:
         out = np.empty((rows, cols), np.float32)
         self._random_matrix(seed, rows, cols, lo, hi, 1 if half else 0, out)
         return out
+
+    def rng_below(self, seed: int, bounds) -> list:
+        """Rng(seed).below(b) for each b in order (include/efta/rng.hpp:31-38)."""
+        n = len(bounds)
+        bb = (C.c_uint32 * max(1, n))(*bounds)
+        out = (C.c_uint32 * max(1, n))()
+        self._below(seed, n, bb, out)
+        return [int(out[i]) for i in range(n)]
 
     def flip_bit(self, v: float, width: int, bit: int) -> float:
         return float(self._flip(v, width, bit))

@@ -75,6 +75,8 @@ typedef struct {
     int P##gen_trial(uint64_t seed, int n, int d, int block, int stride, const int* sites,    \
                      int n_sites, float* q, float* k, float* v, orc_fault_spec* spec_out);    \
     /* Matrix::random(rows, cols, Rng(seed), lo, hi, half_grid ? HALF_STORED : FULL)       */ \
+    /* Rng(seed); out[i] = below(bounds[i]) in order (rng.hpp:31-38; acceptance.cpp:137-156) */ \
+    void P##rng_below_seq(uint64_t seed, int n, const uint32_t* bounds, uint32_t* out);       \
     void P##random_matrix(uint64_t seed, int rows, int cols, double lo, double hi,            \
                           int half_grid, float* out);                                         \
     float P##flip_bit(float v, int width, int bit);                                           \

@@ -92,6 +92,11 @@ int eref_gen_trial(uint64_t seed, int n, int d, int block, int stride, const int
     }
 }
 
+void eref_rng_below_seq(uint64_t seed, int n, const uint32_t* bounds, uint32_t* out) {
+    Rng rng(seed);
+    for (int i = 0; i < n; ++i) out[i] = rng.below(bounds[i]);
+}
+
 void eref_random_matrix(uint64_t seed, int rows, int cols, double lo, double hi, int half_grid,
                         float* out) {
     Rng rng(seed);

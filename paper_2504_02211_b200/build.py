@@ -29,6 +29,8 @@ UNITS = [
     ("efta_capi.cu", []),
     ("efta_attn_inst.cu", ["-DEFTA_INST_D=64"]),
     ("efta_attn_inst.cu", ["-DEFTA_INST_D=128"]),
+    ("efta_attn_inst.cu", ["-DEFTA_INST_D=64", "-DEFTA_INST_INJ=1"]),
+    ("efta_attn_inst.cu", ["-DEFTA_INST_D=128", "-DEFTA_INST_INJ=1"]),
     ("abft_gemm.cu", []),
     ("efta_host.cu", []),
 ]

@@ -106,11 +106,71 @@ def calibrate_thresholds(seq_len, head_dim, mode="efta-opt", trials=64, safety=2
     return thr, rep.family_max
 
 
+def run_fault_records(qs, ks, vs, specs, thr: Thresholds, mode="efta-opt", device="cuda"):
+    """One batched pair of launches (fault-free twin, then faulted) over independent heads:
+    head i gets inputs (qs[i], ks[i], vs[i]) [S, d] fp16 and fault spec specs[i] (or None).
+    Returns per-head records with the reference classify_trial outcome, whether the fault
+    fired, and the non-CLEAN events (kind, block_i, block_j, status, row, col)."""
+    n_rec = len(qs)
+    seq_len, head_dim = qs[0].shape
+    dev = torch.device(device)
+    shape = (1, n_rec, seq_len, head_dim)
+    q = torch.from_numpy(np.stack(qs)).to(dev).view(shape)
+    k = torch.from_numpy(np.stack(ks)).to(dev).view(shape)
+    v = torch.from_numpy(np.stack(vs)).to(dev).view(shape)
+    ev_cap = max(4096, 64 * n_rec)
+    clean = EftaAttention(1, n_rec, seq_len, head_dim, mode=mode, thr=thr, debug=True,
+                          ev_cap=ev_cap, device=dev)
+    o_ref, _, _ = clean(q, k, v)
+    rep_clean = clean.report()
+    faulted = EftaAttention(1, n_rec, seq_len, head_dim, mode=mode, thr=thr, debug=True,
+                            ev_cap=ev_cap, fired_cap=2 * n_rec, device=dev)
+    hspecs = []
+    for i, f in enumerate(specs):
+        if f is not None:
+            hspecs.append(FaultSpec(f.site, f.block_i, f.block_j, f.row, f.col, f.bit, f.trigger, head=i))
+    faulted.set_faults(hspecs)
+    o, m, l = faulted(q, k, v)
+    rep = faulted.report(m, l)
+    det, rr, failed = per_head_report(rep.events, n_rec)
+    fired_heads = {f["spec"].head for f in rep.fired}
+    o_np = o.view(n_rec, seq_len, head_dim).cpu().numpy()
+    r_np = o_ref.view(n_rec, seq_len, head_dim).cpu().numpy()
+    l_np = l.view(n_rec, seq_len).cpu().numpy()
+    events = {i: [] for i in range(n_rec)}
+    corr = [0] * n_rec
+    reco = [0] * n_rec
+    for e in rep.events:
+        h = e["head"]
+        corr[h] += e["corrections"]
+        if e["kind"] in ("exp_checksum", "factor_range") and e["status"] == "corrected":
+            reco[h] += 1
+        if e["status"] != "clean":
+            events[h].append((e["kind"], e["block_i"], e["block_j"], e["status"], e["row"], e["col"]))
+    clean_det = [0] * n_rec
+    for e in rep_clean.events:
+        if e["status"] != "clean":
+            clean_det[e["head"]] += 1
+    out = []
+    for i in range(n_rec):
+        oc = classify(o_np[i], r_np[i], det[i], rr[i], failed[i], l_np[i], specs[i], thr.eps2)
+        res = float(np.abs(o_np[i].astype(np.float64) - r_np[i]).max())
+        ref_inf = float(np.abs(r_np[i]).max())
+        out.append(dict(outcome=oc, fired=i in fired_heads, detections=det[i], corrections=corr[i],
+                        recomputes=reco[i], range_replacements=rr[i], failed=failed[i],
+                        events=sorted(events[i]), clean_false_alarms=clean_det[i],
+                        argmax_ok=rows_argmax_match(o_np[i], r_np[i]), residual_out=res,
+                        rel_residual_out=res / ref_inf if ref_inf > 0 else 0.0))
+    return out
+
+
 def run_gpu_campaign(n_trials=20, heads=12, seq_len=512, head_dim=64, sites=None, seed=7,
                      mode="efta-opt", thr: Thresholds | None = None, calibrate_trials=128,
                      device="cuda", fixed_plan=None):
     """run_campaign (src/campaign.cpp:154-259) with injection: one single-bit
-    fault per (trial, head) record, classified against the fault-free twin."""
+    fault per (trial, head) record, classified against the fault-free twin. Runs the
+    fault-tap build of the production CTA-pair kernel (debug=1) whenever the query-tile
+    count is even."""
     if sites is None:
         sites = list(range(8))
     if thr is None:
@@ -127,56 +187,28 @@ def run_gpu_campaign(n_trials=20, heads=12, seq_len=512, head_dim=64, sites=None
             if fixed_plan is not None:
                 f = FaultSpec.parse(fixed_plan) if isinstance(fixed_plan, str) else fixed_plan
                 f = FaultSpec(f.site, f.block_i, f.block_j, f.row, f.col, f.bit, f.trigger)
-            f.head = t * heads + h
             qs.append(q); ks.append(k); vs.append(v); specs.append(f)
-    dev = torch.device(device)
-    shape = (1, n_rec, seq_len, head_dim)
-    q = torch.from_numpy(np.stack(qs)).to(dev).view(shape)
-    k = torch.from_numpy(np.stack(ks)).to(dev).view(shape)
-    v = torch.from_numpy(np.stack(vs)).to(dev).view(shape)
-    ev_cap = max(4096, 64 * n_rec)
-    clean = EftaAttention(1, n_rec, seq_len, head_dim, mode=mode, thr=thr, debug=True,
-                          ev_cap=ev_cap, device=dev)
-    o_ref, _, _ = clean(q, k, v)
-    rep_clean = clean.report()
-    faulted = EftaAttention(1, n_rec, seq_len, head_dim, mode=mode, thr=thr, debug=True,
-                            ev_cap=ev_cap, fired_cap=2 * n_rec, device=dev)
-    faulted.set_faults(specs)
-    o, m, l = faulted(q, k, v)
-    rep = faulted.report(m, l)
-    det, rr, failed = per_head_report(rep.events, n_rec)
-    fired_heads = {f["spec"].head for f in rep.fired}
-    o_np = o.view(n_rec, seq_len, head_dim).cpu().numpy()
-    r_np = o_ref.view(n_rec, seq_len, head_dim).cpu().numpy()
-    l_np = l.view(n_rec, seq_len).cpu().numpy()
+    recs = run_fault_records(qs, ks, vs, specs, thr, mode, device)
     records = []
     stats = {k2: 0 for k2 in OUTCOMES}
-    corr = [0] * n_rec
-    reco = [0] * n_rec
-    for e in rep.events:
-        corr[e["head"]] += e["corrections"]
-        if e["kind"] in ("exp_checksum", "factor_range") and e["status"] == "corrected":
-            reco[e["head"]] += 1
-    for i in range(n_rec):
-        out = classify(o_np[i], r_np[i], det[i], rr[i], failed[i], l_np[i], specs[i], thr.eps2)
-        stats[out] += 1
-        res = float(np.abs(o_np[i].astype(np.float64) - r_np[i]).max())
-        ref_inf = float(np.abs(r_np[i]).max())
+    for i, r in enumerate(recs):
+        stats[r["outcome"]] += 1
         records.append(dict(trial=i // heads, head=i % heads, seed=seeds[i], injected=True,
-                            fired=i in fired_heads, fault=specs[i].to_string(),
-                            site=SITES[specs[i].site], bit=specs[i].bit, detections=det[i],
-                            corrections=corr[i], recomputes=reco[i], range_replacements=rr[i],
-                            failed=failed[i], argmax_ok=rows_argmax_match(o_np[i], r_np[i]),
-                            residual_out=res, rel_residual_out=res / ref_inf if ref_inf > 0 else 0.0,
-                            outcome=out))
+                            fired=r["fired"], fault=specs[i].to_string(), spec=specs[i],
+                            site=SITES[specs[i].site], bit=specs[i].bit, detections=r["detections"],
+                            corrections=r["corrections"], recomputes=r["recomputes"],
+                            range_replacements=r["range_replacements"], failed=r["failed"],
+                            argmax_ok=r["argmax_ok"], residual_out=r["residual_out"],
+                            rel_residual_out=r["rel_residual_out"], outcome=r["outcome"],
+                            events=r["events"]))
     n_fired = sum(r["fired"] for r in records)
     bad = sum(1 for r in records if r["fired"] and r["outcome"] == "uncorrectable")
     return {"records": n_rec, "fired": n_fired, "coverage": 1.0 - bad / n_fired if n_fired else 1.0,
             "corrected": stats["corrected"], "masked_benign": stats["masked_benign"],
             "range_restricted": stats["range_restricted"],
             "range_contract": stats["range_contract"], "uncorrectable": stats["uncorrectable"],
-            "false_alarms": rep_clean.detections, "thresholds": (thr.eps1, thr.eps2, thr.eps_lin),
-            "detail": records, "events": rep.events}
+            "false_alarms": sum(r["clean_false_alarms"] for r in recs),
+            "thresholds": (thr.eps1, thr.eps2, thr.eps_lin), "detail": records}
 
 
 # ---------------------------------------------------------------- wire formats

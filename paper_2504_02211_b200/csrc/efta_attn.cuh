@@ -133,20 +133,73 @@ struct AttnLayout {
 // trigger semantics mirror FaultInjector::tap (include/efta/fault.hpp:82-95).
 struct ThreadTap {
     int active, site, bj, col, bit, trigger, count, idx;
+    int logged;  // the fired record is written once even if a block is re-evaluated (pair kernel chain redo)
+    __device__ __forceinline__ float fire(const AttnParams& p, float v) {
+        const float flipped = __uint_as_float(__float_as_uint(v) ^ (1u << bit));
+        if (!logged) {
+            logged = 1;
+            const int slot = atomicAdd(&p.counters->n_fired, 1);
+            if (slot < p.fired_cap) {
+                p.fired[slot].spec = p.faults[idx];
+                p.fired[slot].before = v;
+                p.fired[slot].after = flipped;
+            }
+        }
+        return flipped;
+    }
     __device__ __forceinline__ float operator()(const AttnParams& p, int s, int j, int c,
                                                 float v) {
         if (!active || s != site || j != bj || c != col) return v;
         if (++count != trigger) return v;
-        const float flipped = __uint_as_float(__float_as_uint(v) ^ (1u << bit));
-        const int slot = atomicAdd(&p.counters->n_fired, 1);
-        if (slot < p.fired_cap) {
-            p.fired[slot].spec = p.faults[idx];
-            p.fired[slot].before = v;
-            p.fired[slot].after = flipped;
+        return fire(p, v);
+    }
+    // One evaluation of cell `col` of site s at key block j: counts it and returns true
+    // when this evaluation is the trigger-th (the caller then flips that cell with fire()).
+    // Lets an unrolled register row be tapped without dynamic indexing.
+    __device__ __forceinline__ bool hit(int s, int j) {
+        if (!active || s != site || j != bj) return false;
+        return ++count == trigger;
+    }
+    // set up from the device fault table for (head, row-block bi, row); at most one spec
+    // per row-block (src/fault.cpp:117-119), the last match wins like the linear scan
+    __device__ __forceinline__ void load(const AttnParams& p, int head, int bi, int row) {
+        active = 0;
+        count = 0;
+        logged = 0;
+        for (int i = 0; i < p.n_faults; ++i) {
+            const efta_fault_spec f = p.faults[i];
+            if (f.head == head && f.block_i == bi && f.row == row) {
+                active = 1;
+                site = f.site;
+                bj = f.block_j;
+                col = f.col;
+                bit = f.bit;
+                trigger = f.trigger;
+                idx = i;
+            }
         }
-        return flipped;
     }
 };
+
+// value of / store into element `col` of a register row without dynamic indexing (selects;
+// rare-path and tap-build helpers)
+template <int N>
+__device__ __forceinline__ float sel_get(const float* x, int col) {
+    float v = 0.0f;
+#pragma unroll
+    for (int c = 0; c < N; ++c) v = (c == col) ? x[c] : v;
+    return v;
+}
+template <int N>
+__device__ __forceinline__ void sel_set(float* x, int col, float v) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) x[c] = (c == col) ? v : x[c];
+}
+// tap one cell of a register row: counts the evaluation of (site, j, tap.col), flips on trigger
+template <int N>
+__device__ __forceinline__ void tap_row(ThreadTap& tap, const AttnParams& p, int site, int j, float* x) {
+    if (tap.hit(site, j) && tap.col < N) sel_set<N>(x, tap.col, tap.fire(p, sel_get<N>(x, tap.col)));
+}
 
 __device__ __forceinline__ void atomic_max_nonneg(float* addr, float v) {
     if (!(v >= 0.0f)) return;

@@ -35,6 +35,19 @@
 // (warpgroup, warp quarter) an early and a late chain barrier (32 arrivals). Named
 // barriers: warpgroup 0 uses the single-warpgroup ids 1..7, warpgroup 1 the same +
 // kBarAltOfs (9, 10, 11, 14 in the loop; 9, 12, 13, 15 in the epilogue).
+// Tile boundary: the chain slots (early / late / lchain) and the fin slot hold one value
+// each. Warpgroup 0's block 0 of tile k+1 does not depend on warpgroup 1 otherwise, so it
+// waits on `ack` (per warp quarter, arrived by warpgroup 1 once it has read the last chain
+// values and fin of tile k, at its epilogue) before it publishes anything for tile k+1.
+//
+// INJ (fault-tap build, `debug` calls): the same schedule with the reference's explicit op
+// sequence (src/efta.cpp:125-257) so every FaultSite can be tapped by the thread owning the
+// row: GEMM1_OUT on the scaled score, REDUCE_MAX, SUB_MAX, EXP_OUT, REDUCE_SUM on the running
+// denominator, RESCALE_FACTOR / GEMM2_ACC on the O accumulator around the P.V MMAs,
+// NORMALIZE_OUT in the epilogue. Rescaling is eager (P always referenced to the running max,
+// as in the reference), and the running denominator travels along the chain (lchain) so
+// REDUCE_SUM sees the reference's l. A block redone after a chain revision restores the tap's
+// evaluation count first (the reference evaluates each block once).
 #pragma once
 #include "efta_attn_kernel.cuh"
 // included by efta_attn_pair.cuh after PairLayout
@@ -46,9 +59,10 @@ constexpr uint32_t kBarAltOfs = 8;
 struct AltXch {
     float2 early[2][128];  // (m_true, m_run) of the producer warpgroup's last block, fast path
     float2 late[2][128];   // the same after the producer's tile decision / recovery
-    float4 fin[128];       // warpgroup 1 -> 0 after the loop: l, lb, m_ref, m_true
+    float4 fin[128];       // warpgroup 0 -> 1 after the loop: l, lb, m_ref, m_true
+    float lchain[2][128];  // INJ: the reference's running denominator after the producer's block
 };
-static_assert(sizeof(AltXch) == 6144, "PairLayout reserves 6 KB for the chain exchange");
+static_assert(sizeof(AltXch) == 7168, "PairLayout reserves 7 KB for the chain exchange");
 
 // explicit shared-space loads (a generic pointer would compile to the slower generic LD path)
 __device__ __forceinline__ float2 lds_f2(const float2* p) {
@@ -65,15 +79,37 @@ __device__ __forceinline__ float4 lds_f4(const float4* p) {
     return v;
 }
 
-template <int D, bool PROT>
+// observe_linear (efta.cpp:181-185) on the pair kernel: residual max(|d1|, |d2|/G) of the
+// scaled score row against its checksums (c1 from the score MMA, c2 on the CUDA cores)
+template <int D>
+__device__ __noinline__ float pair_linear_residual(const AttnParams& p, const float* sc, const float* c1s,
+                                                   int head, int bi, int j, int row) {
+    float c2s[kStride];
+    pair_score_c2<D>(p, head, bi, j, row, c2s);
+    float lin = 0.0f;
+    for (int x = 0; x < kStride; ++x) {
+        float a = 0.0f, b = 0.0f;
+        for (int l = 0; l < kBlock / kStride; ++l) {
+            a = __fadd_rn(a, sc[x + kStride * l]);
+            b = __fadd_rn(b, __fmul_rn(static_cast<float>(l + 1), sc[x + kStride * l]));
+        }
+        const float d1 = fabsf(c1s[x] - a);
+        const float d2 = fabsf(c2s[x] - b) / static_cast<float>(kBlock / kStride);
+        lin = fmaxf(lin, fmaxf(d1, d2));
+    }
+    return lin;
+}
+
+template <int D, bool PROT, bool INJ>
 __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, uint64_t* s_full,
                                         uint64_t* s_free, uint64_t* p_ready, uint64_t* o_done, uint64_t* o_final,
-                                        uint64_t* mx_early, uint64_t* mx_late, uint64_t* fin_bar,
+                                        uint64_t* mx_early, uint64_t* mx_late, uint64_t* fin_bar, uint64_t* ack_bar,
                                         uint64_t* o_free, uint32_t tmem, int warp, int lane, int n,
                                         const int* tinfo, uint64_t* t_full, uint64_t* t_empty, uint32_t rank) {
     using L = PairLayout<D, PROT>;
+    static_assert(!INJ || PROT, "the fault-tap build is the protected variant");
     constexpr int MODE = PROT ? EFTA_MODE_EFTA_OPT : EFTA_MODE_NONE;
-    constexpr bool kWideTmem = !PROT || D == 64;
+    constexpr bool kWideTmem = (!PROT || D == 64) && !INJ;
     const int w = (warp - 4) >> 2;
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
@@ -86,7 +122,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         rs.ints = reinterpret_cast<int*>(r + 128 * sizeof(RowSlot));
         rs.dbl = reinterpret_cast<double*>(r + 128 * sizeof(RowSlot) + 16 * sizeof(int));
     }
-    ThreadTap tap{};  // inactive: the tap variants run the single-warpgroup kernel
+    ThreadTap tap{};  // INJ: this row's fault spec of the current tile
     uint64_t* my_early = mx_early + w * 4 + wq;
     uint64_t* my_late = mx_late + w * 4 + wq;
     uint64_t* pa_early = mx_early + (1 - w) * 4 + wq;
@@ -94,6 +130,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     const float scale = p.scale, scale_log2 = p.scale_log2;
     const uint32_t s_addr = lane_base + L::COL_S0 + w * L::SW;
     const uint32_t cs_addr = s_addr + 128;  // c1_hi (8) | c1_lo (8)
+    float fam_exp = 0.0f, fam_lin = 0.0f, fam_out = 0.0f;  // worst clean residuals (INJ observation)
 
     // persistent: the (head, query-pair) tiles this cluster draws from the tile ring; every barrier phase runs on the
     // global block counter g = k*n + j (n is even, so block parity = warpgroup)
@@ -104,7 +141,9 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     if (u < 0) break;
     const int head = u / npq, qt = 2 * (u % npq) + static_cast<int>(rank);
     const int seq_row0 = head * p.seq_len;
-    // own sums, referenced to m_ref (the reference max of this warpgroup's last block)
+    if constexpr (INJ) tap.load(p, head, qt, row);
+    // own sums, referenced to m_ref (the reference max of this warpgroup's last block);
+    // INJ: l_w is the reference's full running denominator (lchain)
     float l_w = 0.0f, lb_w = 0.0f, m_ref = -CUDART_INF_F, m_true_last = -CUDART_INF_F;
     for (int j = w; j < n; j += 2, ++it) {
         const int g = k * n + j;
@@ -114,6 +153,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         EFTA_TSQ(8, j);
         tc_fence_after();
         const uint32_t pph = static_cast<uint32_t>((g - 1) >> 1) & 1u;  // partner's phase for block g-1
+        const int tap_snap = tap.count;
         float pv[kBlock];
         float m_true_prev = -CUDART_INF_F, m_run_prev = -CUDART_INF_F;
         float m_true, m_new, bm, psum_f = 0.0f;
@@ -136,15 +176,40 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                 for (int x = 0; x < kStride; ++x)
                     csr[x] = __float_as_uint(__fadd_rn(__uint_as_float(csr[x]), __uint_as_float(csr[kStride + x])));
             }
-            float mx0 = pv[0], mx1 = pv[1], mx2 = pv[2], mx3 = pv[3];
+            int sc_fault_col = -1;
+            float sc_fault_val = 0.0f;
+            if constexpr (INJ) {
+                // reference order: S = scale * (Q K^T) [GEMM1_OUT], row max + bias, running max [REDUCE_MAX]
+                tap.count = tap_snap;
 #pragma unroll
-            for (int c = 4; c < kBlock; c += 4) {
-                mx0 = fmaxf(mx0, pv[c]);
-                mx1 = fmaxf(mx1, pv[c + 1]);
-                mx2 = fmaxf(mx2, pv[c + 2]);
-                mx3 = fmaxf(mx3, pv[c + 3]);
+                for (int c = 0; c < kBlock; ++c) pv[c] = __fmul_rn(pv[c], scale);
+                if (tap.hit(EFTA_GEMM1_OUT, j) && tap.col < kBlock) {
+                    sc_fault_col = tap.col;
+                    sc_fault_val = tap.fire(p, sel_get<kBlock>(pv, sc_fault_col));
+                    sel_set<kBlock>(pv, sc_fault_col, sc_fault_val);
+                }
+                if (p.observe_linear && attempt == 0) {
+                    float c1s[kStride];
+#pragma unroll
+                    for (int x = 0; x < kStride; ++x) c1s[x] = __fmul_rn(__uint_as_float(csr[x]), scale);
+                    const float lin = pair_linear_residual<D>(p, pv, c1s, head, qt, j, row);
+                    if (isfinite(lin)) fam_lin = fmaxf(fam_lin, lin);
+                }
+                float b = pv[0];
+#pragma unroll
+                for (int c = 1; c < kBlock; ++c) b = (b < pv[c]) ? pv[c] : b;
+                bm = b + p.rowmax_bias;
+            } else {
+                float mx0 = pv[0], mx1 = pv[1], mx2 = pv[2], mx3 = pv[3];
+#pragma unroll
+                for (int c = 4; c < kBlock; c += 4) {
+                    mx0 = fmaxf(mx0, pv[c]);
+                    mx1 = fmaxf(mx1, pv[c + 1]);
+                    mx2 = fmaxf(mx2, pv[c + 2]);
+                    mx3 = fmaxf(mx3, pv[c + 3]);
+                }
+                bm = __fmul_rn(fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)), scale) + p.rowmax_bias;
             }
-            bm = __fmul_rn(fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)), scale) + p.rowmax_bias;
             // ---- the max chain: block j-1 belongs to the partner warpgroup
             if (j > 0) {
                 if (attempt == 0) {
@@ -159,14 +224,21 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                 }
             }
             m_true = (m_true_prev < bm) ? bm : m_true_prev;
-            m_new = (j == 0 || m_true - m_run_prev > kLazyTau) ? m_true : m_run_prev;
+            if constexpr (INJ) {
+                m_new = m_true;  // eager: P is always referenced to the running max
+                if (tap.hit(EFTA_REDUCE_MAX, j) && tap.col == 0) m_new = tap.fire(p, m_new);
+                m_true = m_new;
+            } else {
+                m_new = (j == 0 || m_true - m_run_prev > kLazyTau) ? m_true : m_run_prev;
+            }
             if (attempt == 0) {
+                // tile boundary: warpgroup 1 has consumed the previous tile's chain / fin slots
+                if (w == 0 && j == 0 && k > 0) mbar_wait(&ack_bar[wq], static_cast<uint32_t>(k - 1) & 1u);
                 xc->early[w][row] = make_float2(m_true, m_new);
                 mbar_arrive(my_early);
             }
             if ((warp & 3) == 0) EFTA_TS(15, j);
             EFTA_TSQ(4, j);
-            const float mL = m_new * kLog2e;
             float pc1v[kStride];
             float2 prod_f[kStride / 2];
             if (PROT) {
@@ -175,43 +247,73 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                 for (int x = 0; x < kStride; ++x)
                     pc1v[x] = ex2_approx(__fsub_rn(__fmul_rn(__uint_as_float(csr[x]), scale), g16m) * kLog2e);
             }
-            const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
             float2 ps0 = make_float2(0.0f, 0.0f), ps1 = make_float2(0.0f, 0.0f);
+            if constexpr (INJ) {
+                // P = exp(S - m) with the SUB_MAX / EXP_OUT taps (src/efta.cpp:161-170)
 #pragma unroll
-            for (int c = 0; c < kBlock; c += 2) {
-                const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
-                float2 e;
-                if (exp_on_fma<D>(c)) {
-                    e = ex2_poly2(a);
-                } else {
-                    e.x = ex2_approx(a.x);
-                    e.y = ex2_approx(a.y);
+                for (int c = 0; c < kBlock; ++c) pv[c] = __fsub_rn(pv[c], m_new);
+                tap_row<kBlock>(tap, p, EFTA_SUB_MAX, j, pv);
+#pragma unroll
+                for (int c = 0; c < kBlock; ++c) pv[c] = ex2_approx(pv[c] * kLog2e);
+                tap_row<kBlock>(tap, p, EFTA_EXP_OUT, j, pv);
+#pragma unroll
+                for (int c = 0; c < kBlock; c += 2) {
+                    const float2 e = make_float2(pv[c], pv[c + 1]);
+                    if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
+                    else ps0 = fadd2(ps0, e);
+                    const int gg = (c & 7) >> 1;
+                    prod_f[gg] = (c < kStride) ? e : fmul2(prod_f[gg], e);
                 }
-                pv[c] = e.x;
-                pv[c + 1] = e.y;
-                if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
-                else ps0 = fadd2(ps0, e);
-                if (PROT) {
-                    const int g = (c & 7) >> 1;
-                    prod_f[g] = (c < kStride) ? e : fmul2(prod_f[g], e);
+            } else {
+                const float mL = m_new * kLog2e;
+                const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
+#pragma unroll
+                for (int c = 0; c < kBlock; c += 2) {
+                    const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
+                    float2 e;
+                    if (exp_on_fma<D>(c)) {
+                        e = ex2_poly2(a);
+                    } else {
+                        e.x = ex2_approx(a.x);
+                        e.y = ex2_approx(a.y);
+                    }
+                    pv[c] = e.x;
+                    pv[c + 1] = e.y;
+                    if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
+                    else ps0 = fadd2(ps0, e);
+                    if (PROT) {
+                        const int gg = (c & 7) >> 1;
+                        prod_f[gg] = (c < kStride) ? e : fmul2(prod_f[gg], e);
+                    }
                 }
             }
             psum_f = (ps0.x + ps0.y) + (ps1.x + ps1.y);
             if (!PROT) break;  // no recovery path: the chain can never be revised
 
-            // ---- exp-domain strided product check (see row_wg) + factor guard
+            // ---- exp-domain strided product check (see row_wg) + factor guard. A row is
+            // degenerate where the reference's log test is undefined: P or Pc1 not finite and
+            // positive (snvr.cpp:18,55-66), read off the group products
             const float f = ex2_approx((m_run_prev - m_new) * kLog2e);
             bool exp_affected = false;
             int exp_viol = 0;
             bool degenerate = !isfinite(m_new);
+            float exp_res = 0.0f;
 #pragma unroll
             for (int x = 0; x < kStride; ++x) {
                 const float pr = (x & 1) ? prod_f[x >> 1].y : prod_f[x >> 1].x;
-                const bool bad = !(pr >= pc1v[x] * p.exp_lo && pr <= pc1v[x] * p.exp_hi);
+                const float pc1 = pc1v[x];
+                // the bracket flags every degenerate group except P = Pc1 = 0 and P = Pc1 = inf
+                const bool bad = !(pr > 0.0f && pc1 < CUDART_INF_F && pr >= pc1 * p.exp_lo && pr <= pc1 * p.exp_hi);
+                if constexpr (INJ) {
+                    if (!(pr > 0.0f && pr < CUDART_INF_F) || !(pc1 > 0.0f && pc1 < CUDART_INF_F))
+                        degenerate = true;
+                    else
+                        exp_res = fmaxf(exp_res, fabsf(lg2_approx(__fdividef(pr, pc1))) * kLn2);
+                }
                 if (bad) { exp_affected = true; ++exp_viol; }
             }
-            float exp_res = 0.0f;
             if (degenerate) { exp_affected = true; exp_res = CUDART_INF_F; exp_viol = 1; }
+            if (INJ && attempt == 0 && isfinite(exp_res)) fam_exp = fmaxf(fam_exp, exp_res);
             const bool factor_bad = (j > 0) && !(f > 0.0f && f <= 1.0f);
             // ---- late chain check: did the partner's decision revise block j-1's maxima?
             bool chain_bad = false;
@@ -227,33 +329,32 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             if (!named_bar_or(6 + bo, 128, exp_affected || factor_bad || chain_bad)) break;
             if (named_bar_or(6 + bo, 128, chain_bad)) continue;  // redo the block with the revised maxima
             // ---- rare: the reference recovery ladder for this tile
+            if constexpr (!INJ) {
+                // the event's first-look residual: inf for a degenerate row (snvr.cpp:55-66)
+#pragma unroll
+                for (int x = 0; x < kStride; ++x) {
+                    const float pr = (x & 1) ? prod_f[x >> 1].y : prod_f[x >> 1].x;
+                    if (!(pr > 0.0f && pr < CUDART_INF_F) || !(pc1v[x] > 0.0f && pc1v[x] < CUDART_INF_F))
+                        degenerate = true;
+                }
+                if (degenerate) { exp_res = CUDART_INF_F; exp_viol = 1; }
+            }
             float p_loc[kBlock];
 #pragma unroll
             for (int c = 0; c < kBlock; ++c) p_loc[c] = pv[c];
             int replaced = 0;
-            exp_stage_slow<false, D, true>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res, exp_viol,
-                                  m_run_prev, m_new, bm, p_loc, replaced, tap, -1, 0.0f, rs, bo);
+            exp_stage_slow<INJ, D, true>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res, exp_viol,
+                                         m_run_prev, m_new, bm, p_loc, replaced, tap, sc_fault_col, sc_fault_val,
+                                         rs, bo);
             if (replaced) {
 #pragma unroll
                 for (int c = 0; c < kBlock; ++c) pv[c] = p_loc[c];
             }
             replaced_p = replaced != 0;
             m_true = (m_true_prev < m_new) ? m_new : m_true_prev;
+            if (INJ) m_true = m_new;
             break;
         }
-        if (PROT) {
-            xc->late[w][row] = make_float2(m_true, m_new);
-            mbar_arrive(my_late);
-        }
-        // S_j is no longer read: the score MMA of block j+2 may overwrite S[w]
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&s_free[w], 0);
-        if ((warp & 3) == 0) EFTA_TS(2, j);
-        // ---- factors: fo for the shared O accumulator (chain), fw for this warpgroup's sums
-        const float fo = ex2_approx((m_run_prev - m_new) * kLog2e);
-        const float fw = ex2_approx((m_ref - m_new) * kLog2e);
-        if (PROT) lb_w = __fadd_rn(__fmul_rn(lb_w, fw), ex2_approx((bm - m_new) * kLog2e));
         float psum = psum_f;
         if (replaced_p) {
             float2 ps0 = make_float2(pv[0], pv[1]), ps1 = make_float2(pv[2], pv[3]);
@@ -264,7 +365,29 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             }
             psum = (ps0.x + ps0.y) + (ps1.x + ps1.y);
         }
-        l_w = __fadd_rn(__fmul_rn(fw, l_w), psum);
+        // ---- factors: fo for the shared O accumulator (chain), fw for this warpgroup's sums
+        const float fo = ex2_approx((m_run_prev - m_new) * kLog2e);
+        const float fw = ex2_approx((m_ref - m_new) * kLog2e);
+        if constexpr (INJ) {
+            // the reference's running denominator l = f * l_prev + rowsum(P) [REDUCE_SUM]
+            // (src/efta.cpp:244-250); l_prev is the partner's, read under the late barrier
+            const float lprev = (j > 0) ? xc->lchain[1 - w][row] : 0.0f;
+            float lv = __fadd_rn(__fmul_rn(fo, lprev), psum);
+            if (tap.hit(EFTA_REDUCE_SUM, j) && tap.col == 0) lv = tap.fire(p, lv);
+            l_w = lv;
+            xc->lchain[w][row] = lv;
+        }
+        if (PROT) {
+            xc->late[w][row] = make_float2(m_true, m_new);
+            mbar_arrive(my_late);
+        }
+        // S_j is no longer read: the score MMA of block j+2 may overwrite S[w]
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&s_free[w], 0);
+        if ((warp & 3) == 0) EFTA_TS(2, j);
+        if (PROT) lb_w = __fadd_rn(__fmul_rn(lb_w, fw), ex2_approx((bm - m_new) * kLog2e));
+        if constexpr (!INJ) l_w = __fadd_rn(__fmul_rn(fw, l_w), psum);
 
         if ((warp & 3) == 0) EFTA_TS(3, j);
         // ---- P (fp16): packed first, stored once the P buffer is free (P.V of block j-1
@@ -272,7 +395,17 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         uint32_t pk[64];
 #pragma unroll
         for (int x = 0; x < 64; ++x) pk[x] = pack_half2(pv[2 * x], pv[2 * x + 1]);
-        const bool need_o = j > 0 && !__all_sync(0xffffffffu, fo == 1.0f);
+        bool need_o = j > 0 && !__all_sync(0xffffffffu, fo == 1.0f);
+        // INJ: the O accumulator taps of this block force the rescale pass: GEMM2_ACC of block
+        // j-1 (after its P.V), RESCALE_FACTOR of block j, and of block 0 (deferred to block 1:
+        // P.V(0) overwrites the accumulator, so the tapped zero is added after it)
+        bool t_res0 = false;
+        if constexpr (INJ) {
+            const bool t_acc = j > 0 && tap.active && tap.site == EFTA_GEMM2_ACC && tap.bj == j - 1;
+            const bool t_res = j > 0 && tap.active && tap.site == EFTA_RESCALE_FACTOR && tap.bj == j;
+            t_res0 = j == 1 && tap.active && tap.site == EFTA_RESCALE_FACTOR && tap.bj == 0;
+            need_o = need_o || __any_sync(0xffffffffu, t_acc || t_res || t_res0);
+        }
         if (L::NPB == 1 ? (g > 0) : (g >= 2 || need_o)) {
             if ((warp & 3) == 0) EFTA_TS(4, j);
             if (L::NPB == 1 || need_o)
@@ -292,23 +425,27 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         // P.V of block j-1 is complete (waited above)
         if (need_o) {
             constexpr int NCH = D / 32 + (PROT ? 1 : 0);
-            float o[NCH][32];
+            float o[NCH * 32];
 #pragma unroll
             for (int c = 0; c < NCH; ++c)
-                tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
+                tmem_ld32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
             tmem_wait_ld();
+            if constexpr (INJ) {
+                if (t_res0 && tap.hit(EFTA_RESCALE_FACTOR, 0) && tap.col < D)
+                    sel_set<D>(o, tap.col, __fadd_rn(sel_get<D>(o, tap.col), tap.fire(p, 0.0f)));
+                tap_row<D>(tap, p, EFTA_GEMM2_ACC, j - 1, o);
+            }
             const float2 f2 = make_float2(fo, fo);
 #pragma unroll
-            for (int c = 0; c < NCH; ++c)
+            for (int x = 0; x < NCH * 32; x += 2) {
+                const float2 r2 = fmul2(make_float2(o[x], o[x + 1]), f2);
+                o[x] = r2.x;
+                o[x + 1] = r2.y;
+            }
+            if constexpr (INJ) tap_row<D>(tap, p, EFTA_RESCALE_FACTOR, j, o);
 #pragma unroll
-                for (int x = 0; x < 32; x += 2) {
-                    const float2 r2 = fmul2(make_float2(o[c][x], o[c][x + 1]), f2);
-                    o[c][x] = r2.x;
-                    o[c][x + 1] = r2.y;
-                }
-#pragma unroll
             for (int c = 0; c < NCH; ++c)
-                tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c][0]));
+                tmem_st32(lane_base + L::COL_O + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
         }
         tmem_wait_st();
         tc_fence_before();
@@ -323,12 +460,13 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     // Warpgroup 1 ran the tile's last block (n is even): it merges the sums and runs the
     // epilogue while warpgroup 0 already starts the next tile.
     if (w == 0) {
-        xc->fin[row] = make_float4(l_w, lb_w, m_ref, m_true_last);
+        xc->fin[row] = make_float4(INJ ? 0.0f : l_w, lb_w, m_ref, m_true_last);
         mbar_arrive(&fin_bar[wq]);
         continue;
     }
     mbar_wait(&fin_bar[wq], static_cast<uint32_t>(k) & 1u);
     const float4 fb = lds_f4(&xc->fin[row]);
+    mbar_arrive(&ack_bar[wq]);  // this tile's chain and fin slots are consumed
     float m_run = m_ref;  // the chain's final reference max (block n-1 is ours)
     const float m_true = m_true_last;
     const float fbf = ex2_approx((fb.z - m_run) * kLog2e);
@@ -358,6 +496,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive_cluster(o_free, 0);
+    if constexpr (INJ) tap_row<D>(tap, p, EFTA_GEMM2_ACC, n - 1, o);
     {
         // bring O, its checksums, l and the lower bound from the lazy reference max to
         // the row's true max (the reference's final m); F == 1 for most rows
@@ -372,7 +511,6 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         }
         m_run = m_true;
     }
-    float fam_out = 0.0f;
     double eps_mult = 1.0;
     if (PROT) {
         // denominator range restriction (snvr.cpp:161-182, efta.cpp:289-310)
@@ -410,17 +548,27 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         }
     }
     // normalization (efta.cpp:312-327): one IEEE reciprocal, then products (within 1 ulp of
-    // the reference's division; the tap kernel keeps the exact division)
-    const float rl = __frcp_rn(l_run);
+    // the reference's division); the tap build keeps the reference's division [NORMALIZE_OUT]
+    if constexpr (INJ) {
 #pragma unroll
-    for (int c = 0; c < D; c += 2) {
-        const float2 r2 = fmul2(make_float2(o[c], o[c + 1]), make_float2(rl, rl));
-        o[c] = r2.x;
-        o[c + 1] = r2.y;
+        for (int c = 0; c < D; ++c) o[c] = __fdiv_rn(o[c], l_run);
+        tap_row<D>(tap, p, EFTA_NORMALIZE_OUT, 0, o);
+#pragma unroll
+        for (int x = 0; x < kStride; ++x) { c1[x] = __fdiv_rn(c1[x], l_run); c2[x] = __fdiv_rn(c2[x], l_run); }
+    } else {
+        const float rl = __frcp_rn(l_run);
+#pragma unroll
+        for (int c = 0; c < D; c += 2) {
+            const float2 r2 = fmul2(make_float2(o[c], o[c + 1]), make_float2(rl, rl));
+            o[c] = r2.x;
+            o[c + 1] = r2.y;
+        }
+        if (PROT) {
+#pragma unroll
+            for (int x = 0; x < kStride; ++x) { c1[x] = __fmul_rn(c1[x], rl); c2[x] = __fmul_rn(c2[x], rl); }
+        }
     }
     if (PROT) {
-#pragma unroll
-        for (int x = 0; x < kStride; ++x) { c1[x] = __fmul_rn(c1[x], rl); c2[x] = __fmul_rn(c2[x], rl); }
         float res;
         verify_output_tile<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res, bo);
         if (isfinite(res)) fam_out = fmaxf(fam_out, res);
@@ -431,12 +579,26 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
     if (p.m_out) p.m_out[grow] = m_run;
     if (p.l_out) p.l_out[grow] = l_run;
-    if (PROT) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) fam_out = fmaxf(fam_out, __shfl_xor_sync(0xffffffffu, fam_out, off));
-        if (lane == 0) atomic_max_nonneg(&p.counters->family_max[1], fam_out);
-    }
     }  // tiles
+    if (PROT) {
+        // per-family worst clean residuals (calibration / observation): exp and linear
+        // families from both warpgroups (INJ only), output from the epilogue warpgroup
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            fam_out = fmaxf(fam_out, __shfl_xor_sync(0xffffffffu, fam_out, off));
+            if (INJ) {
+                fam_exp = fmaxf(fam_exp, __shfl_xor_sync(0xffffffffu, fam_exp, off));
+                fam_lin = fmaxf(fam_lin, __shfl_xor_sync(0xffffffffu, fam_lin, off));
+            }
+        }
+        if (lane == 0) {
+            if (w == 1) atomic_max_nonneg(&p.counters->family_max[1], fam_out);
+            if (INJ) {
+                atomic_max_nonneg(&p.counters->family_max[0], fam_exp);
+                if (p.observe_linear) atomic_max_nonneg(&p.counters->family_max[2], fam_lin);
+            }
+        }
+    }
     (void)MODE;
 }
 

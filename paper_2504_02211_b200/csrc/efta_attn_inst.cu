@@ -1,6 +1,9 @@
+// efta_attn_inst.cu — instantiations of the fused attention kernels for one head dim
+// (EFTA_INST_D). EFTA_INST_INJ=1 builds only the fault-tap variant of the CTA-pair kernel
+// (its own translation unit so the variants compile in parallel); otherwise the unit holds
+// the single-CTA kernel (all modes x {fast, tap}), the fast pair kernels and the prepass.
 #include <algorithm>
-// efta_attn_inst.cu — instantiations of the fused attention kernel for one head
-// dim (EFTA_INST_D), all modes x {fast, debug/tap} variants.
+
 #include "efta_attn_kernel.cuh"
 #include "efta_attn_pair.cuh"
 #include "efta_launch.h"
@@ -8,24 +11,46 @@
 #ifndef EFTA_INST_D
 #error "EFTA_INST_D must be 64 or 128"
 #endif
+#ifndef EFTA_INST_INJ
+#define EFTA_INST_INJ 0
+#endif
 
 using namespace efta_sm100;
 
 namespace {
 
+// The dynamic shared-memory limit is a per-device function attribute: set it on every
+// launch (cheap, thread-safe, correct when one process drives several GPUs).
+template <typename K>
+cudaError_t set_smem(K kern, uint32_t bytes) {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
+
+template <int D, int MODE, bool INJ>
+cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const CUtensorMap& tkb,
+                          const CUtensorMap& tkc, const CUtensorMap& tvt, const AttnParams& p, int bh,
+                          cudaStream_t st) {
+    using PL = PairLayout<D, MODE != 0>;
+    auto kern = efta_attn_pair_kernel<D, MODE, INJ>;
+    if (cudaError_t e = set_smem(kern, PL::SMEM_BYTES)) return e;
+    int dev = 0, nsm = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return e;
+    if (cudaError_t e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) return e;
+    const int tiles = bh * (p.nblk / 2);  // (head, query pair) tiles
+    const int ncl = std::min(tiles, std::max(1, nsm / 2));
+    dim3 grid(2 * ncl);
+    kern<<<grid, kPairThreads, PL::SMEM_BYTES, st>>>(tq, tka, tkb, tkc, tvt, p);
+    return cudaGetLastError();
+}
+
+#if !EFTA_INST_INJ
 template <int D, int MODE, bool DBG>
 cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const CUtensorMap& tkc, const CUtensorMap& tvc, const AttnParams& p, int bh,
                      cudaStream_t st) {
     using L = AttnLayout<D>;
     auto kern = efta_attn_fwd_kernel<D, MODE, DBG>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             L::SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    if (cudaError_t e = set_smem(kern, L::SMEM_BYTES)) return e;
     dim3 grid(p.nblk, bh);
     kern<<<grid, 256, L::SMEM_BYTES, st>>>(tq, tk, tv, tkc, tvc, p);
     return cudaGetLastError();
@@ -45,83 +70,51 @@ cudaError_t launch_d(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMa
     }
 }
 
-template <int D, int MODE>
-cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const CUtensorMap& tkb,
-                          const CUtensorMap& tkc, const CUtensorMap& tvt, const AttnParams& p, int bh,
-                          cudaStream_t st) {
-    using PL = PairLayout<D, MODE != 0>;
-    auto kern = efta_attn_pair_kernel<D, MODE>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int tiles = bh * (p.nblk / 2);  // (head, query pair) tiles
-    const int ncl = std::min(tiles, std::max(1, nsm / 2));
-    dim3 grid(2 * ncl);
-    kern<<<grid, kPairThreads, PL::SMEM_BYTES, st>>>(tq, tka, tkb, tkc, tvt, p);
+template <int D>
+cudaError_t launch_encode_pair(bool prot, const void* k, const void* v, void* kc, void* vt, int seq_len, int nblk,
+                               int bh, cudaStream_t st) {
+    dim3 grid(nblk, bh);
+    auto kh = static_cast<const __half*>(k);
+    auto vh = static_cast<const __half*>(v);
+    if (prot)
+        efta_encode_pair_kernel<D, true><<<grid, 256, 0, st>>>(kh, vh, static_cast<__half*>(kc),
+                                                              static_cast<__half*>(vt), seq_len, nblk);
+    else
+        efta_encode_pair_kernel<D, false><<<grid, 256, 0, st>>>(kh, vh, static_cast<__half*>(kc),
+                                                               static_cast<__half*>(vt), seq_len, nblk);
     return cudaGetLastError();
-}
-
-}  // namespace
-
-#if EFTA_INST_D == 64
-cudaError_t efta_launch_attn_d64(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMap& tk,
-                                 const CUtensorMap& tv, const CUtensorMap& tkc,
-                                 const CUtensorMap& tvc, const AttnParams& p, int bh,
-                                 cudaStream_t st) {
-    return launch_d<64>(mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
-}
-#else
-cudaError_t efta_launch_attn_d128(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMap& tk,
-                                  const CUtensorMap& tv, const CUtensorMap& tkc,
-                                  const CUtensorMap& tvc, const AttnParams& p, int bh,
-                                  cudaStream_t st) {
-    return launch_d<128>(mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
 }
 #endif
 
-#if EFTA_INST_D == 64
-cudaError_t efta_launch_attn_pair_d64(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
-                                      const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
-                                      const AttnParams& p, int bh, cudaStream_t st) {
-    return mode == 0 ? launch_pair_t<64, 0>(tq, tka, tkb, tkc, tvt, p, bh, st)
-                     : launch_pair_t<64, 2>(tq, tka, tkb, tkc, tvt, p, bh, st);
-}
-cudaError_t efta_launch_encode_pair_d64(bool prot, const void* k, const void* v, void* kc, void* vt,
-                                        int seq_len, int nblk, int bh, cudaStream_t st) {
-    dim3 grid(nblk, bh);
-    if (prot)
-        efta_encode_pair_kernel<64, true><<<grid, 256, 0, st>>>(static_cast<const __half*>(k), static_cast<const __half*>(v),
-                                                             static_cast<__half*>(kc), static_cast<__half*>(vt), seq_len, nblk);
-    else
-        efta_encode_pair_kernel<64, false><<<grid, 256, 0, st>>>(static_cast<const __half*>(k), static_cast<const __half*>(v),
-                                                              static_cast<__half*>(kc), static_cast<__half*>(vt), seq_len, nblk);
-    return cudaGetLastError();
+}  // namespace
+
+#define EFTA_CAT2(a, b) a##b
+#define EFTA_CAT(a, b) EFTA_CAT2(a, b)
+#define EFTA_SFX EFTA_CAT(_d, EFTA_INST_D)
+
+#if EFTA_INST_INJ
+cudaError_t EFTA_CAT(efta_launch_attn_pair_inj, EFTA_SFX)(const CUtensorMap& tq, const CUtensorMap& tka,
+                                                         const CUtensorMap& tkb, const CUtensorMap& tkc,
+                                                         const CUtensorMap& tvt, const AttnParams& p, int bh,
+                                                         cudaStream_t st) {
+    return launch_pair_t<EFTA_INST_D, EFTA_MODE_EFTA_OPT, true>(tq, tka, tkb, tkc, tvt, p, bh, st);
 }
 #else
-cudaError_t efta_launch_attn_pair_d128(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
-                                       const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
-                                       const AttnParams& p, int bh, cudaStream_t st) {
-    return mode == 0 ? launch_pair_t<128, 0>(tq, tka, tkb, tkc, tvt, p, bh, st)
-                     : launch_pair_t<128, 2>(tq, tka, tkb, tkc, tvt, p, bh, st);
+cudaError_t EFTA_CAT(efta_launch_attn, EFTA_SFX)(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMap& tk,
+                                                const CUtensorMap& tv, const CUtensorMap& tkc,
+                                                const CUtensorMap& tvc, const AttnParams& p, int bh,
+                                                cudaStream_t st) {
+    return launch_d<EFTA_INST_D>(mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
 }
-cudaError_t efta_launch_encode_pair_d128(bool prot, const void* k, const void* v, void* kc, void* vt,
-                                         int seq_len, int nblk, int bh, cudaStream_t st) {
-    dim3 grid(nblk, bh);
-    if (prot)
-        efta_encode_pair_kernel<128, true><<<grid, 256, 0, st>>>(static_cast<const __half*>(k), static_cast<const __half*>(v),
-                                                              static_cast<__half*>(kc), static_cast<__half*>(vt), seq_len, nblk);
-    else
-        efta_encode_pair_kernel<128, false><<<grid, 256, 0, st>>>(static_cast<const __half*>(k), static_cast<const __half*>(v),
-                                                               static_cast<__half*>(kc), static_cast<__half*>(vt), seq_len, nblk);
-    return cudaGetLastError();
+cudaError_t EFTA_CAT(efta_launch_attn_pair, EFTA_SFX)(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
+                                                     const CUtensorMap& tkb, const CUtensorMap& tkc,
+                                                     const CUtensorMap& tvt, const AttnParams& p, int bh,
+                                                     cudaStream_t st) {
+    return mode == 0 ? launch_pair_t<EFTA_INST_D, 0, false>(tq, tka, tkb, tkc, tvt, p, bh, st)
+                     : launch_pair_t<EFTA_INST_D, 2, false>(tq, tka, tkb, tkc, tvt, p, bh, st);
+}
+cudaError_t EFTA_CAT(efta_launch_encode_pair, EFTA_SFX)(bool prot, const void* k, const void* v, void* kc, void* vt,
+                                                       int seq_len, int nblk, int bh, cudaStream_t st) {
+    return launch_encode_pair<EFTA_INST_D>(prot, k, v, kc, vt, seq_len, nblk, bh, st);
 }
 #endif

@@ -49,13 +49,13 @@ struct PairLayout {
     static constexpr uint32_t OFF_BAR = OFF_V + VS * V_STAGE;
     // q_full, k_full/empty[KS], v_full/empty[VS], s_full[2], s_free[2], p_ready[2],
     // o_done[2], o_final, chain barriers mx_early[2][4], mx_late[2][4], q_empty[2], o_free, fin[4],
-    // second q_full, tile ring full[4] / empty[4]
-    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2 + 2 + 2 + 1 + 16 + 2 + 1 + 4 + 1 + 8;
+    // second q_full, tile ring full[4] / empty[4], tile-boundary ack[4]
+    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2 + 2 + 2 + 1 + 16 + 2 + 1 + 4 + 1 + 8 + 4;
     static constexpr uint32_t OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
     static constexpr uint32_t RED_BYTES = 128 * 24 + 256;  // per row warpgroup
     static constexpr uint32_t OFF_XCH = OFF_RED + 2 * RED_BYTES;
-    static constexpr uint32_t OFF_TINFO = OFF_XCH + 6144;  // tile ring: int[4]
+    static constexpr uint32_t OFF_TINFO = OFF_XCH + 7168;  // tile ring: int[4]
     static constexpr uint32_t SMEM_BYTES = OFF_TINFO + 16 + 1024;
     // TMEM columns
     static constexpr uint32_t COL_S0 = 0, COL_O = 2 * SW, COL_P = COL_O + VROWS, TMEM_COLS = 512;
@@ -169,7 +169,9 @@ namespace efta_sm100 {
 
 // tm_ka: K rows [0, HN_S) (or [64r, 64r+64) unprotected), tm_kb: K rows 72..127 (protected),
 // tm_kc: KC rows in 8-row boxes (protected), tm_vt: [V^T ; VC^T] rows of each block, box rows HN_V.
-template <int D, int MODE>
+// INJ: the fault-tap build (reference op sequence, eager rescale, taps at every FaultSite;
+// efta_attn_alt.cuh) — the `debug` variant of the same schedule.
+template <int D, int MODE, bool INJ>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_ka,
                       const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_kc,
@@ -199,6 +201,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     uint64_t* q_full2 = fin_bar + 4;   // q_full of Q buffer 1 (q_full is buffer 0's)
     uint64_t* t_full = q_full2 + 1;    // [4] tile ring slot published (this CTA)
     uint64_t* t_empty = t_full + 4;    // [4] tile ring slot consumed by all 21 warps (leader)
+    uint64_t* ack_bar = t_empty + 4;   // [4] warpgroup 1 consumed the tile's chain / fin slots (per warp quarter)
     int* tinfo = reinterpret_cast<int*>(smem + L::OFF_TINFO);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
@@ -226,7 +229,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         mbar_init(q_full2, 1);
         for (int i = 0; i < kTileRing; ++i) { mbar_init(&t_full[i], 1); mbar_init(&t_empty[i], kTileConsumers); }
         mbar_init(o_free, 8);
-        for (int i = 0; i < 4; ++i) mbar_init(&fin_bar[i], 32);
+        for (int i = 0; i < 4; ++i) { mbar_init(&fin_bar[i], 32); mbar_init(&ack_bar[i], 32); }
         fence_barrier_init();
         tma_prefetch_desc(&tm_q);
         tma_prefetch_desc(&tm_ka);
@@ -417,9 +420,9 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         __syncwarp();
     } else {
         setmaxnreg_inc<232>();
-        row_alt<D, PROT>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH), s_full, s_free,
-                         p_ready, o_done, o_final, mx_early, mx_late, fin_bar, o_free, tmem, warp, lane, n,
-                         tinfo, t_full, t_empty, rank);
+        row_alt<D, PROT, INJ>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH), s_full,
+                              s_free, p_ready, o_done, o_final, mx_early, mx_late, fin_bar, ack_bar, o_free, tmem,
+                              warp, lane, n, tinfo, t_full, t_empty, rank);
     }
 
     tc_fence_before();

@@ -109,10 +109,14 @@ WsLayout ws_layout(const efta_attn_desc* d) {
 }
 size_t ws_bytes(const efta_attn_desc* d) { return ws_layout(d).total; }
 
-// the fast unprotected / EFTA-optimized variants run on CTA pairs (cta_group::2)
+// Unprotected / EFTA-optimized calls run on CTA pairs (cta_group::2) whenever the number of
+// query tiles is even; the `debug` (fault-tap / observation) calls of EFTA_OPT run the tap
+// build of the same pair kernel. The single-CTA kernel serves mode EFTA (per-iteration output
+// check), odd tile counts, debug calls in mode NONE, and EFTA_NO_PAIR=1 A/B runs.
 bool use_pair(const efta_attn_desc* d) {
-    return !d->debug && d->mode != EFTA_MODE_EFTA && ((d->seq_len / kBlock) % 2) == 0 &&
-           std::getenv("EFTA_NO_PAIR") == nullptr;
+    if (d->mode == EFTA_MODE_EFTA || ((d->seq_len / kBlock) % 2) != 0) return false;
+    if (d->debug && d->mode != EFTA_MODE_EFTA_OPT) return false;
+    return std::getenv("EFTA_NO_PAIR") == nullptr;
 }
 
 int encode_kv(const efta_attn_desc* d, const void* k, const void* v, void* kc, void* vc,
@@ -265,7 +269,10 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     cudaError_t e;
     if (pair)  // the persistent pair kernel's in-order tile counter (workspace scratch, int)
         CUDA_TRY(cudaMemsetAsync(wsb + wl.scratch, 0, 16, st));
-    if (pair)  // maps: q, K half A, K half B (protected peer), KC, [V^T ; VC^T]
+    if (pair && dbg)  // the tap build: maps as below
+        e = (D == 64) ? efta_launch_attn_pair_inj_d64(tq, tk, tv, tkc, tvc, p, bh, st)
+                      : efta_launch_attn_pair_inj_d128(tq, tk, tv, tkc, tvc, p, bh, st);
+    else if (pair)  // maps: q, K half A, K half B (protected peer), KC, [V^T ; VC^T]
         e = (D == 64) ? efta_launch_attn_pair_d64(d->mode, tq, tk, tv, tkc, tvc, p, bh, st)
                       : efta_launch_attn_pair_d128(d->mode, tq, tk, tv, tkc, tvc, p, bh, st);
     else
@@ -299,7 +306,12 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
             for (auto& e : ev) if (e) cudaEventDestroy(e);
         }
     };
-    thread_local Scratch s;
+    // per thread and device (streams and buffers belong to the device current at the call)
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(2, "efta_attn_fwd_host_f16: device index out of range");
+    thread_local Scratch scratch_per_dev[64];
+    Scratch& s = scratch_per_dev[dev];
     if (!s.st[0]) {
         for (auto& x : s.st) CUDA_TRY(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
         for (auto& e : s.ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -351,6 +363,7 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
         CUDA_TRY(cudaStreamWaitEvent(comp, s.ev[2 * c], 0));
         efta_attn_desc dcc = *d;
         if (nchunk > 1) { dcc.batch = 1; dcc.heads = nh; }
+        dcc.checksums_ready = 0;  // the internal workspace never holds this call's operands
         efta_counters* cc = reinterpret_cast<efta_counters*>(reinterpret_cast<char*>(dcnt) + c * cnt_stride);
         efta_event* ce = reinterpret_cast<efta_event*>(reinterpret_cast<char*>(de) + c * ev_stride);
         int rc = efta_attn_fwd_f16(&dcc, dq + e0, dk + e0, dv + e0, dout + e0, dm + r0, dl + r0, dws, wsb,

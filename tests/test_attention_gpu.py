@@ -95,3 +95,53 @@ def test_persistent_pair_many_tiles(d):
     for h in (0, heads - 1):
         ref = orc.efta_forward(q[h], k[h], v[h], 128, 8, mode="none")
         assert rel_err(o_p[h], ref.o) <= TOL, (h, rel_err(o_p[h], ref.o))
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_pair_two_blocks_many_tiles(d):
+    """S = 256 (two key blocks: warpgroup 0 owns block 0, warpgroup 1 block 1 + the epilogue) on
+    256 heads = 256 tiles over <= 74 clusters: warpgroup 0 reaches the next tile's block 0 while
+    warpgroup 1 is still in the previous tile, so the chain / fin hand-over slots are only safe
+    behind the tile-boundary ack barrier. Parity with the oracle on sampled heads, protected ==
+    unprotected bit for bit, and the fault-tap build agrees within tolerance."""
+    from paper_2504_02211_b200 import EftaAttention, Thresholds
+    heads, seq = 256, 256
+    q, k, v, _ = head_inputs(2024 + d, heads, seq, d)
+    qd, kd, vd = (_dev(x)[None] for x in (q, k, v))
+    thr = Thresholds(1e-4, 1e-3, 1e-3)
+    outs = {}
+    for name, mode, dbg in (("opt", "efta-opt", False), ("none", "none", False), ("tap", "efta-opt", True)):
+        op = EftaAttention(1, heads, seq, d, mode=mode, thr=thr, debug=dbg)
+        o, m, l = op(qd, kd, vd)
+        rep = op.report()
+        assert rep.detections == 0 and not rep.failed, (name, rep.events[:3])
+        outs[name] = (o.cpu().numpy()[0], m.cpu().numpy()[0], l.cpu().numpy()[0])
+    assert np.array_equal(outs["opt"][0].view(np.uint32), outs["none"][0].view(np.uint32))
+    orc = oracle()
+    for h in (0, 77, 150, heads - 1):
+        ref = orc.efta_forward(q[h], k[h], v[h], 128, 8, mode="none")
+        for name in outs:
+            assert rel_err(outs[name][0][h], ref.o) <= TOL, (name, h)
+            assert np.allclose(outs[name][1][h], ref.m, rtol=1e-5, atol=1e-5), (name, h)
+            assert np.allclose(outs[name][2][h], ref.l, rtol=1e-3), (name, h)
+
+
+@pytest.mark.parametrize("d,seq", [(64, 512), (128, 1024)])
+def test_tap_build_clean_parity(d, seq):
+    """The fault-tap build of the pair kernel (debug=1: reference op sequence, eager rescale,
+    l along the chain) matches the oracle's O, m and l on clean inputs and stays silent."""
+    from paper_2504_02211_b200 import efta_forward, Thresholds
+    heads = 6
+    q, k, v, _ = head_inputs(555 + d, heads, seq, d)
+    o, rep = efta_forward(_dev(q), _dev(k), _dev(v), mode="efta-opt", thr=Thresholds(1e-4, 1e-3, 1e-3),
+                          debug=True)
+    o = o.cpu().numpy()
+    m = rep.final_m.cpu().numpy()
+    l = rep.final_l.cpu().numpy()
+    orc = oracle()
+    for h in range(heads):
+        ref = orc.efta_forward(q[h], k[h], v[h], 128, 8, mode="efta-opt", thr=(1e-4, 1e-3, 1e-3))
+        assert rel_err(o[h], ref.o) <= TOL
+        assert np.allclose(m[h], ref.m, rtol=1e-5, atol=1e-5)
+        assert np.allclose(l[h], ref.l, rtol=1e-3)
+    assert rep.detections == 0 and not rep.failed
