@@ -20,7 +20,11 @@
  *   efta_abft_gemm_f16       efta::checksummed_gemm + verify_locate_correct
  *                            include/efta/abft.hpp:58-60, 73-77 (strided-ABFT GEMM,
  *                            applied per 256-wide output column tile = FFN linear)
+ *   efta_abft_gemm_ex        the same with an fp32 product and the tile checksums returned
+ *                            (the drop-in checksummed_gemm, abft.hpp:73-77)
  *   efta_abft_encode_weight_f16  encode_strided of a weight matrix, abft.hpp:38
+ *   efta_encode_strided_f32  encode_strided on a device tile, abft.hpp:38
+ *   efta_verify_locate_correct_f32  verify_locate_correct on a device tile, abft.hpp:58-60
  *   efta_flip_bit            efta::flip_bit                 include/efta/fault.hpp:33
  */
 #ifndef EFTA_B200_H
@@ -109,6 +113,32 @@ int efta_abft_gemm_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_
                        const uint16_t* wcs, uint16_t* y, const efta_fault_spec* faults,
                        int n_faults, efta_event* events, int ev_cap, efta_counters* counters,
                        void* stream);
+
+/* Same GEMM with the output in fp32 (y_f32 = 1; the reference's checksummed_gemm returns an
+ * fp32 product) and, if y_checksums != NULL, the tensor-core checksums of every 256-wide output
+ * tile: y_checksums[(row * n/256 + tile) * 16 + {0..7, 8..15}] = c1[x], c2[x]. */
+int efta_abft_gemm_ex(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w,
+                      const uint16_t* wcs, void* y, int y_f32, float* y_checksums,
+                      const efta_fault_spec* faults, int n_faults, efta_event* events, int ev_cap,
+                      efta_counters* counters, void* stream);
+
+/* ---- standalone strided ABFT on a device tile (reference abft.hpp:38-60) ----
+ * encode_strided (src/abft.cpp:19-42): c1/c2 [rows, stride] of an fp32 tile [rows, cols].
+ * verify_locate_correct (src/abft.cpp:65-187): repairs t in place, writes the report to device
+ * memory; row_eps_mult is an optional device array of `rows` doubles. workspace: device buffer
+ * of efta_verify_workspace_bytes(rows) bytes. */
+typedef struct {
+    int status, row, col, violations, corrections, checksum_repair;
+    double residual, delta;
+} efta_verify_report;
+
+int efta_encode_strided_f32(int rows, int cols, int stride, const float* t, float* c1, float* c2,
+                            void* stream);
+size_t efta_verify_workspace_bytes(int rows);
+int efta_verify_locate_correct_f32(int rows, int cols, int stride, float* t, const float* c1,
+                                   const float* c2, double eps, const double* row_eps_mult,
+                                   efta_verify_report* report, void* workspace,
+                                   size_t workspace_bytes, void* stream);
 
 /* ---- host-side helpers of the reference campaign (host memory only) ---- */
 /* trial_seed (include/efta/rng.hpp:55-58) */

@@ -15,6 +15,10 @@
 //                                   include/efta/fault.hpp:16-103
 //   Rng / trial_seed                include/efta/rng.hpp:19-58
 //   classify_trial / Outcome        include/efta/campaign.hpp:12-20, 84-85
+//   calibrate_thresholds / CalibrationResult / threshold_sweep / SweepPoint
+//                                   include/efta/campaign.hpp:87-111
+//   ChecksumPair / encode_strided / verify_locate_correct / checksummed_gemm / GemmStage
+//                                   include/efta/abft.hpp:31-77, include/efta/gemm.hpp:10
 #pragma once
 
 #include <cstdint>
@@ -133,6 +137,19 @@ private:
     std::vector<FiredFault> fired_;
 };
 
+// Analytic operation counters of the CPU reference (include/efta/counters.hpp:13-38). The GPU
+// path reports measured time and ncu profiles instead: accepted for signature compatibility,
+// never written.
+struct Counters {};
+enum class GemmStage { PLAIN, SCORES, OUTPUT };
+
+// Row-direction strided checksums of a tile (include/efta/abft.hpp:31-36)
+struct ChecksumPair {
+    Matrix c1, c2;
+    int stride = 0;
+    int groups = 0;
+};
+
 struct VerificationReport {
     VerifyStatus status = VerifyStatus::CLEAN;
     int row = -1, col = -1;
@@ -163,15 +180,55 @@ struct KernelKnobs {
     float rowmax_bias = 0.0f;
 };
 
+// inj != nullptr (also with an empty plan, e.g. for a fault-free twin) runs the fault-tap build
+// of the kernel (the reference op sequence with eager rescaling); without one, the production
+// build (identical decisions, lazily rescaled accumulator: outputs agree to rounding).
 std::pair<Matrix, FTReport> efta_forward(const Matrix& q, const Matrix& k, const Matrix& v,
                                          const AttnConfig& cfg, const Thresholds& thr, FTMode mode,
                                          FaultInjector* inj = nullptr,
                                          const KernelKnobs* knobs = nullptr);
+
+// ---- strided ABFT primitives (include/efta/abft.hpp:38-77), computed on the GPU ----
+// encode_strided: c1/c2 (rows x stride) of t, fp32 sums in the reference's order (bit-exact).
+ChecksumPair encode_strided(const Matrix& t, int stride, Counters* cnt = nullptr);
+// verify_locate_correct: the reference's detection / location / repair ladder on t (repaired
+// in place) with the reference's report; std::invalid_argument on shape mismatch.
+VerificationReport verify_locate_correct(Matrix& t, const ChecksumPair& cp, double eps_abs,
+                                         Counters* cnt = nullptr,
+                                         const std::vector<double>* row_eps_mult = nullptr);
+// checksummed_gemm: a (M x K) times bt (K x W) on the tcgen05 strided-ABFT GEMM (fp16 operands,
+// inputs on the fp16 grid; fp32 accumulation and product) with the product's strided checksum
+// pair over the full width W carried by the tensor cores (per 256-wide tile, recombined).
+// c_init / cp_init (O += P.V) are added on the device. This kernel's geometry:
+// stride 8, M % 128 == 0, W % 256 == 0, K % 64 == 0 (std::invalid_argument otherwise).
+std::pair<Matrix, ChecksumPair> checksummed_gemm(const Matrix& a, const Matrix& bt, int stride,
+                                                 Counters* cnt = nullptr,
+                                                 GemmStage stage = GemmStage::SCORES,
+                                                 const Matrix* c_init = nullptr,
+                                                 const ChecksumPair* cp_init = nullptr);
 
 enum class Outcome { CLEAN, FALSE_ALARM, CORRECTED, RANGE_RESTRICTED, MASKED_BENIGN,
                      RANGE_CONTRACT, UNCORRECTABLE };
 const char* outcome_name(Outcome o);
 Outcome classify_trial(const Matrix& out, const Matrix& ref, const FTReport& rep,
                        const FaultPlan& plan, const Thresholds& thr);
+
+// calibrate_thresholds (src/campaign.cpp:261-297): clean runs in observation mode on the GPU
+// (one batched launch over the trials), each threshold = worst clean residual x safety.
+struct CalibrationResult {
+    Thresholds thr;
+    double max_exp = 0.0, max_out = 0.0, max_lin = 0.0;
+    bool degenerate = false;
+};
+CalibrationResult calibrate_thresholds(const AttnConfig& cfg, FTMode mode, int trials, double safety,
+                                       uint64_t seed);
+
+// threshold_sweep (src/campaign.cpp:299-357): per trial one clean and one randomly faulted
+// observation run; detection / false-alarm rates re-judged at log-spaced multiples of `base`.
+struct SweepPoint {
+    double multiplier = 0.0, detection_rate = 0.0, false_alarm_rate = 0.0;
+};
+std::vector<SweepPoint> threshold_sweep(const AttnConfig& cfg, FTMode mode, const Thresholds& base,
+                                        int trials, uint64_t seed, int points = 10);
 
 }  // namespace efta_b200

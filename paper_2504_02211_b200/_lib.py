@@ -92,7 +92,8 @@ EXPORTS = ["efta_last_error", "efta_attn_validate", "efta_attn_workspace_bytes",
            "efta_attn_fwd_f16", "efta_attn_fwd_host_f16", "efta_attn_encode_kv_f16",
            "efta_flip_bit", "efta_abft_gemm_f16", "efta_abft_encode_weight_f16",
            "efta_abft_weight_cs_bytes", "efta_trial_seed", "efta_gen_trial_f16",
-           "efta_classify_trial"]
+           "efta_classify_trial", "efta_abft_gemm_ex", "efta_encode_strided_f32",
+           "efta_verify_workspace_bytes", "efta_verify_locate_correct_f32"]
 
 
 def last_error() -> str:

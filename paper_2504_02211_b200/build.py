@@ -32,6 +32,7 @@ UNITS = [
     ("efta_attn_inst.cu", ["-DEFTA_INST_D=64", "-DEFTA_INST_INJ=1"]),
     ("efta_attn_inst.cu", ["-DEFTA_INST_D=128", "-DEFTA_INST_INJ=1"]),
     ("abft_gemm.cu", []),
+    ("abft_verify.cu", []),
     ("efta_host.cu", []),
 ]
 

@@ -51,7 +51,8 @@ constexpr int GEMM_THREADS = 384;  // warps 0-3: TMA / MMA / idle / idle; 4-11: 
 struct GemmParams {
     int m, n, k, m_tiles, n_tiles, k_chunks;
     double eps;
-    __half* y;
+    void* y;        // [m, n] fp16 (or fp32 with the F32 output variant)
+    float* ycs;     // optional [m, n_tiles, 16]: the tile's c1[8], c2[8] per output row (tensor-core checksums)
     const efta_fault_spec* faults;  // site ignored; block_i = global row, col = global col
     int n_faults;
     efta_event* events;
@@ -65,7 +66,7 @@ struct RowScratchG {
     double* dbl;
 };
 
-template <bool DBG>
+template <bool DBG, bool F32>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                  const __grid_constant__ CUtensorMap tm_wc, const GemmParams p) {
@@ -174,7 +175,8 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
             float s1[8], s2[8];
 #pragma unroll
             for (int x = 0; x < 8; ++x) { s1[x] = 0.0f; s2[x] = 0.0f; }
-            __half* yrow = p.y + static_cast<size_t>(grow) * p.n + nt * GN;
+            __half* yrow = static_cast<__half*>(p.y) + static_cast<size_t>(grow) * p.n + nt * GN;
+            float* yrow32 = static_cast<float*>(p.y) + static_cast<size_t>(grow) * p.n + nt * GN;
             // this half's 128 accumulator columns into registers (one wait for all four loads)
             float v[128];
 #pragma unroll
@@ -202,6 +204,12 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
             }
             // fp16 output of this half: packed and stored once the accumulator is released
             auto store_half = [&]() {
+                if constexpr (F32) {
+                    float4* dst = reinterpret_cast<float4*>(yrow32 + half * 128);
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) dst[x] = make_float4(v[4 * x], v[4 * x + 1], v[4 * x + 2], v[4 * x + 3]);
+                    return;
+                }
 #pragma unroll
                 for (int c4 = 0; c4 < 4; ++c4) {
                     uint4 pk[4];
@@ -258,6 +266,13 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                 viol |= fabs(d1) > p.eps || fabs(d2) > p.eps * 32.0;
             }
             fam = fmaxf(fam, static_cast<float>(res));
+            if (p.ycs) {
+                float4* cs = reinterpret_cast<float4*>(p.ycs + (static_cast<size_t>(grow) * p.n_tiles + nt) * 16);
+                cs[0] = make_float4(c1[0], c1[1], c1[2], c1[3]);
+                cs[1] = make_float4(c1[4], c1[5], c1[6], c1[7]);
+                cs[2] = make_float4(c2[0], c2[1], c2[2], c2[3]);
+                cs[3] = make_float4(c2[4], c2[5], c2[6], c2[7]);
+            }
             const bool tile_cs_bad = named_bar_or(4, 128, cs_bad);
             const bool any = named_bar_or(5, 128, viol || cs_bad);
             if (row == 0) *dec = any ? 1 : 0;
@@ -292,8 +307,10 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                         for (int c = 0; c < GN; ++c) before[c] = tloc[c];
                         verify_row<GN>(tloc, c1, c2, p.eps, rv);
                         for (int c = 0; c < GN; ++c)
-                            if (__float_as_uint(tloc[c]) != __float_as_uint(before[c]))
-                                yrow[c] = __float2half_rn(tloc[c]);
+                            if (__float_as_uint(tloc[c]) != __float_as_uint(before[c])) {
+                                if constexpr (F32) yrow32[c] = tloc[c];
+                                else yrow[c] = __float2half_rn(tloc[c]);
+                            }
                     }
                 }
                 TileReport tr = reduce_tile_report(rv, tile_cs_bad, row, rs.slots, rs.ints, rs.dbl);
@@ -416,9 +433,9 @@ int efta_abft_encode_weight_f16(const efta_gemm_desc* d, const uint16_t* w, uint
     return e == cudaSuccess ? 0 : gfail(2, cudaGetErrorString(e));
 }
 
-int efta_abft_gemm_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w,
-                       const uint16_t* wcs, uint16_t* y, const efta_fault_spec* faults, int n_faults,
-                       efta_event* events, int ev_cap, efta_counters* counters, void* stream) {
+int efta_abft_gemm_ex(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w, const uint16_t* wcs, void* y,
+                      int y_f32, float* y_checksums, const efta_fault_spec* faults, int n_faults, efta_event* events,
+                      int ev_cap, efta_counters* counters, void* stream) {
     if (int rc = gvalidate(d)) return rc;
     if (!x || !w || !wcs || !y || !counters) return gfail(1, "abft_gemm: null buffer");
     if (n_faults > 0 && !d->debug) return gfail(1, "abft_gemm: fault injection needs debug=1");
@@ -437,7 +454,8 @@ int efta_abft_gemm_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_
     p.n_tiles = d->n / GN;
     p.k_chunks = d->k / GK;
     p.eps = d->eps;
-    p.y = reinterpret_cast<__half*>(y);
+    p.y = y;
+    p.ycs = y_checksums;
     p.faults = faults;
     p.n_faults = faults ? n_faults : 0;
     p.events = events;
@@ -454,8 +472,17 @@ int efta_abft_gemm_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_
         kern<<<grid, GEMM_THREADS, SMEM_BYTES, st>>>(tx, tw, twc, p);
         return cudaGetLastError();
     };
-    e = d->debug ? launch(abft_gemm_kernel<true>) : launch(abft_gemm_kernel<false>);
+    if (y_f32)
+        e = d->debug ? launch(abft_gemm_kernel<true, true>) : launch(abft_gemm_kernel<false, true>);
+    else
+        e = d->debug ? launch(abft_gemm_kernel<true, false>) : launch(abft_gemm_kernel<false, false>);
     return e == cudaSuccess ? 0 : gfail(2, cudaGetErrorString(e));
+}
+
+int efta_abft_gemm_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w,
+                       const uint16_t* wcs, uint16_t* y, const efta_fault_spec* faults, int n_faults,
+                       efta_event* events, int ev_cap, efta_counters* counters, void* stream) {
+    return efta_abft_gemm_ex(d, x, w, wcs, y, 0, nullptr, faults, n_faults, events, ev_cap, counters, stream);
 }
 
 }  // extern "C"

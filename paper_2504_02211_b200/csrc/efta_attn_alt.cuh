@@ -130,7 +130,28 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     const float scale = p.scale, scale_log2 = p.scale_log2;
     const uint32_t s_addr = lane_base + L::COL_S0 + w * L::SW;
     const uint32_t cs_addr = s_addr + 128;  // c1_hi (8) | c1_lo (8)
-    float fam_exp = 0.0f, fam_lin = 0.0f, fam_out = 0.0f;  // worst clean residuals (INJ observation)
+    float fam_exp = 0.0f, fam_lin = 0.0f;  // INJ observation: worst clean exp / linear residuals
+    // per-family worst clean residuals, flushed per tile (nothing extra stays live across tiles)
+    auto flush_families = [&](float fam_out) {
+        if (!PROT) return;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            fam_out = fmaxf(fam_out, __shfl_xor_sync(0xffffffffu, fam_out, off));
+            if (INJ) {
+                fam_exp = fmaxf(fam_exp, __shfl_xor_sync(0xffffffffu, fam_exp, off));
+                fam_lin = fmaxf(fam_lin, __shfl_xor_sync(0xffffffffu, fam_lin, off));
+            }
+        }
+        if (lane == 0) {
+            if (w == 1) atomic_max_nonneg(&p.counters->family_max[1], fam_out);
+            if (INJ) {
+                atomic_max_nonneg(&p.counters->family_max[0], fam_exp);
+                if (p.observe_linear) atomic_max_nonneg(&p.counters->family_max[2], fam_lin);
+            }
+        }
+        fam_exp = 0.0f;
+        fam_lin = 0.0f;
+    };
 
     // persistent: the (head, query-pair) tiles this cluster draws from the tile ring; every barrier phase runs on the
     // global block counter g = k*n + j (n is even, so block parity = warpgroup)
@@ -302,8 +323,9 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             for (int x = 0; x < kStride; ++x) {
                 const float pr = (x & 1) ? prod_f[x >> 1].y : prod_f[x >> 1].x;
                 const float pc1 = pc1v[x];
-                // the bracket flags every degenerate group except P = Pc1 = 0 and P = Pc1 = inf
-                const bool bad = !(pr > 0.0f && pc1 < CUDART_INF_F && pr >= pc1 * p.exp_lo && pr <= pc1 * p.exp_hi);
+                // strict bounds: P = Pc1 = 0 and P = Pc1 = inf fail them like every other
+                // degenerate group; a tie at a finite bound has measure zero
+                const bool bad = !(pr > pc1 * p.exp_lo && pr < pc1 * p.exp_hi);
                 if constexpr (INJ) {
                     if (!(pr > 0.0f && pr < CUDART_INF_F) || !(pc1 > 0.0f && pc1 < CUDART_INF_F))
                         degenerate = true;
@@ -355,28 +377,28 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             if (INJ) m_true = m_new;
             break;
         }
-        float psum = psum_f;
-        if (replaced_p) {
+        // the partial row sum of P (re-summed with the fast path's pairing after a recompute)
+        auto row_psum = [&]() {
+            if (!replaced_p) return psum_f;
             float2 ps0 = make_float2(pv[0], pv[1]), ps1 = make_float2(pv[2], pv[3]);
 #pragma unroll
             for (int c = 4; c < kBlock; c += 4) {
                 ps0 = fadd2(ps0, make_float2(pv[c], pv[c + 1]));
                 ps1 = fadd2(ps1, make_float2(pv[c + 2], pv[c + 3]));
             }
-            psum = (ps0.x + ps0.y) + (ps1.x + ps1.y);
-        }
-        // ---- factors: fo for the shared O accumulator (chain), fw for this warpgroup's sums
-        const float fo = ex2_approx((m_run_prev - m_new) * kLog2e);
-        const float fw = ex2_approx((m_ref - m_new) * kLog2e);
+            return (ps0.x + ps0.y) + (ps1.x + ps1.y);
+        };
         if constexpr (INJ) {
             // the reference's running denominator l = f * l_prev + rowsum(P) [REDUCE_SUM]
             // (src/efta.cpp:244-250); l_prev is the partner's, read under the late barrier
+            const float f_l = ex2_approx((m_run_prev - m_new) * kLog2e);
             const float lprev = (j > 0) ? xc->lchain[1 - w][row] : 0.0f;
-            float lv = __fadd_rn(__fmul_rn(fo, lprev), psum);
+            float lv = __fadd_rn(__fmul_rn(f_l, lprev), row_psum());
             if (tap.hit(EFTA_REDUCE_SUM, j) && tap.col == 0) lv = tap.fire(p, lv);
             l_w = lv;
             xc->lchain[w][row] = lv;
         }
+        // publish first: the partner's next block and the score MMA of block j+2 wait on these
         if (PROT) {
             xc->late[w][row] = make_float2(m_true, m_new);
             mbar_arrive(my_late);
@@ -386,8 +408,11 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&s_free[w], 0);
         if ((warp & 3) == 0) EFTA_TS(2, j);
+        // ---- factors: fo for the shared O accumulator (chain), fw for this warpgroup's sums
+        const float fo = ex2_approx((m_run_prev - m_new) * kLog2e);
+        const float fw = ex2_approx((m_ref - m_new) * kLog2e);
         if (PROT) lb_w = __fadd_rn(__fmul_rn(lb_w, fw), ex2_approx((bm - m_new) * kLog2e));
-        if constexpr (!INJ) l_w = __fadd_rn(__fmul_rn(fw, l_w), psum);
+        if constexpr (!INJ) l_w = __fadd_rn(__fmul_rn(fw, l_w), row_psum());
 
         if ((warp & 3) == 0) EFTA_TS(3, j);
         // ---- P (fp16): packed first, stored once the P buffer is free (P.V of block j-1
@@ -462,6 +487,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     if (w == 0) {
         xc->fin[row] = make_float4(INJ ? 0.0f : l_w, lb_w, m_ref, m_true_last);
         mbar_arrive(&fin_bar[wq]);
+        if (INJ) flush_families(0.0f);
         continue;
     }
     mbar_wait(&fin_bar[wq], static_cast<uint32_t>(k) & 1u);
@@ -568,10 +594,11 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             for (int x = 0; x < kStride; ++x) { c1[x] = __fmul_rn(c1[x], rl); c2[x] = __fmul_rn(c2[x], rl); }
         }
     }
+    float fam_out = 0.0f;
     if (PROT) {
         float res;
         verify_output_tile<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res, bo);
-        if (isfinite(res)) fam_out = fmaxf(fam_out, res);
+        if (isfinite(res)) fam_out = res;
     }
     const size_t grow = static_cast<size_t>(seq_row0) + qt * kBlock + row;
     float4* dst = reinterpret_cast<float4*>(p.o + grow * D);
@@ -579,26 +606,8 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
     if (p.m_out) p.m_out[grow] = m_run;
     if (p.l_out) p.l_out[grow] = l_run;
+    flush_families(fam_out);
     }  // tiles
-    if (PROT) {
-        // per-family worst clean residuals (calibration / observation): exp and linear
-        // families from both warpgroups (INJ only), output from the epilogue warpgroup
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            fam_out = fmaxf(fam_out, __shfl_xor_sync(0xffffffffu, fam_out, off));
-            if (INJ) {
-                fam_exp = fmaxf(fam_exp, __shfl_xor_sync(0xffffffffu, fam_exp, off));
-                fam_lin = fmaxf(fam_lin, __shfl_xor_sync(0xffffffffu, fam_lin, off));
-            }
-        }
-        if (lane == 0) {
-            if (w == 1) atomic_max_nonneg(&p.counters->family_max[1], fam_out);
-            if (INJ) {
-                atomic_max_nonneg(&p.counters->family_max[0], fam_exp);
-                if (p.observe_linear) atomic_max_nonneg(&p.counters->family_max[2], fam_lin);
-            }
-        }
-    }
     (void)MODE;
 }
 

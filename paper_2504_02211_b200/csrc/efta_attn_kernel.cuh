@@ -522,7 +522,7 @@ __device__ __forceinline__ void row_wg(const AttnParams& p, uint8_t* red, uint64
                 const float pr = (x & 1) ? prod[x >> 1].y : prod[x >> 1].x;
                 const float c1s = __fmul_rn(__uint_as_float(csr[x]), scale);
                 const float pc1 = DBG ? ex2_approx(__fsub_rn(c1s, g16m) * kLog2e) : pc1v[x];
-                const bool bad = !(pr >= pc1 * p.exp_lo && pr <= pc1 * p.exp_hi);
+                const bool bad = !(pr > pc1 * p.exp_lo && pr < pc1 * p.exp_hi);  // strict: also fails 0/0, inf/inf
                 if (DBG) {
                     if (!(pr > 0.0f && pr < CUDART_INF_F) || !(pc1 > 0.0f && pc1 < CUDART_INF_F)) {
                         degenerate = true;

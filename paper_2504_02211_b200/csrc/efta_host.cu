@@ -8,6 +8,10 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <stdexcept>
+#include <vector>
+
+#include <cuda_runtime.h>
 
 #include "../../include/efta_b200.h"
 #include "../../include/efta_b200.hpp"
@@ -220,7 +224,8 @@ std::pair<Matrix, FTReport> efta_forward(const Matrix& q, const Matrix& k, const
     desc.eps_lin = thr.eps_lin;
     desc.observe_linear = knobs && knobs->observe_linear;
     desc.rowmax_bias = knobs ? knobs->rowmax_bias : 0.0f;
-    desc.debug = (inj && !inj->plan().empty()) || desc.observe_linear;
+    // an injector (even with an empty plan: a fault-free twin) selects the fault-tap build
+    desc.debug = inj != nullptr || desc.observe_linear;
     std::vector<uint16_t> hq(static_cast<size_t>(n) * d), hk(hq.size()), hv(hq.size());
     for (size_t i = 0; i < hq.size(); ++i) {
         hq[i] = to_half_bits(q.data()[i]);
@@ -288,6 +293,262 @@ std::pair<Matrix, FTReport> efta_forward(const Matrix& q, const Matrix& k, const
         }
     }
     return {std::move(out), std::move(rep)};
+}
+
+// ------------------------------------------------------------------ strided ABFT on the GPU
+namespace {
+
+// device buffer owned by one drop-in call (the C-ABI itself never allocates)
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(size_t bytes) {
+        if (bytes && cudaMalloc(&p, bytes) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+void cuda_check(cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+}
+void capi_check(int rc) {
+    if (rc == 1) throw std::invalid_argument(efta_last_error());
+    if (rc != 0) throw std::runtime_error(efta_last_error());
+}
+
+// full-width checksums of a product from its per-256-column-tile ones:
+//   c1 = sum_t c1_t,  c2 = sum_t (c2_t + 32 t c1_t)   (group index l = 32 t + l')
+// and, when given, the accumulated pair of C = C_init + A.B (checksummed_gemm's cp_init)
+__global__ void compose_tile_checksums(int rows, int tiles, const float* __restrict__ ycs,
+                                       const float* __restrict__ init1, const float* __restrict__ init2,
+                                       float* __restrict__ c1, float* __restrict__ c2) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * 8) return;
+    const int r = i / 8, x = i % 8;
+    float a = 0.0f, b = 0.0f;
+    for (int t = 0; t < tiles; ++t) {
+        const float* cs = ycs + (static_cast<size_t>(r) * tiles + t) * 16;
+        a = __fadd_rn(a, cs[x]);
+        b = __fadd_rn(b, __fadd_rn(cs[8 + x], __fmul_rn(32.0f * t, cs[x])));
+    }
+    if (init1) {
+        a = __fadd_rn(init1[i], a);
+        b = __fadd_rn(init2[i], b);
+    }
+    c1[i] = a;
+    c2[i] = b;
+}
+__global__ void add_into(size_t n, const float* __restrict__ src, float* __restrict__ dst) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = __fadd_rn(src[i], dst[i]);
+}
+
+}  // namespace
+
+ChecksumPair encode_strided(const Matrix& t, int stride, Counters*) {
+    if (stride <= 0 || t.cols() % stride != 0)
+        throw std::invalid_argument("encode_strided: stride must divide tile width");
+    ChecksumPair cp;
+    cp.stride = stride;
+    cp.groups = t.cols() / stride;
+    cp.c1 = Matrix(t.rows(), stride);
+    cp.c2 = Matrix(t.rows(), stride);
+    const size_t nt = static_cast<size_t>(t.rows()) * t.cols(), nc = static_cast<size_t>(t.rows()) * stride;
+    DevBuf dt(nt * 4), d1(nc * 4), d2(nc * 4);
+    cuda_check(cudaMemcpy(dt.p, t.data(), nt * 4, cudaMemcpyHostToDevice));
+    capi_check(efta_encode_strided_f32(t.rows(), t.cols(), stride, dt.as<float>(), d1.as<float>(), d2.as<float>(),
+                                       nullptr));
+    cuda_check(cudaMemcpy(cp.c1.data(), d1.p, nc * 4, cudaMemcpyDeviceToHost));
+    cuda_check(cudaMemcpy(cp.c2.data(), d2.p, nc * 4, cudaMemcpyDeviceToHost));
+    return cp;
+}
+
+VerificationReport verify_locate_correct(Matrix& t, const ChecksumPair& cp, double eps_abs, Counters*,
+                                         const std::vector<double>* row_eps_mult) {
+    const int rows = t.rows(), stride = cp.stride;
+    if (stride <= 0 || t.cols() != stride * cp.groups || cp.c1.rows() != rows || cp.c2.rows() != rows ||
+        cp.c1.cols() != stride || cp.c2.cols() != stride)
+        throw std::invalid_argument("verify_locate_correct: checksum/tile shape mismatch");
+    if (row_eps_mult && static_cast<int>(row_eps_mult->size()) != rows)
+        throw std::invalid_argument("verify_locate_correct: row_eps_mult size mismatch");
+    VerificationReport rep;
+    if (rows == 0) return rep;
+    const size_t nt = static_cast<size_t>(rows) * t.cols(), nc = static_cast<size_t>(rows) * stride;
+    const size_t ws = efta_verify_workspace_bytes(rows);
+    DevBuf dt(nt * 4), d1(nc * 4), d2(nc * 4), dm(row_eps_mult ? rows * sizeof(double) : 0),
+        dr(sizeof(efta_verify_report)), dws(ws);
+    cuda_check(cudaMemcpy(dt.p, t.data(), nt * 4, cudaMemcpyHostToDevice));
+    cuda_check(cudaMemcpy(d1.p, cp.c1.data(), nc * 4, cudaMemcpyHostToDevice));
+    cuda_check(cudaMemcpy(d2.p, cp.c2.data(), nc * 4, cudaMemcpyHostToDevice));
+    if (row_eps_mult)
+        cuda_check(cudaMemcpy(dm.p, row_eps_mult->data(), rows * sizeof(double), cudaMemcpyHostToDevice));
+    capi_check(efta_verify_locate_correct_f32(rows, t.cols(), stride, dt.as<float>(), d1.as<float>(),
+                                              d2.as<float>(), eps_abs, row_eps_mult ? dm.as<double>() : nullptr,
+                                              dr.as<efta_verify_report>(), dws.p, ws, nullptr));
+    efta_verify_report r{};
+    cuda_check(cudaMemcpy(&r, dr.p, sizeof r, cudaMemcpyDeviceToHost));
+    cuda_check(cudaMemcpy(t.data(), dt.p, nt * 4, cudaMemcpyDeviceToHost));
+    rep.status = static_cast<VerifyStatus>(r.status);
+    rep.row = r.row;
+    rep.col = r.col;
+    rep.violations = r.violations;
+    rep.corrections = r.corrections;
+    rep.checksum_repair = r.checksum_repair != 0;
+    rep.residual = r.residual;
+    rep.delta = r.delta;
+    return rep;
+}
+
+std::pair<Matrix, ChecksumPair> checksummed_gemm(const Matrix& a, const Matrix& bt, int stride, Counters*,
+                                                 GemmStage, const Matrix* c_init, const ChecksumPair* cp_init) {
+    const int m = a.rows(), k = a.cols(), w = bt.cols();
+    if (bt.rows() != k) throw std::invalid_argument("checksummed_gemm: inner dimensions differ");
+    if (stride <= 0 || w % stride != 0) throw std::invalid_argument("encode_strided: stride must divide tile width");
+    if (stride != 8 || m % 128 || w % 256 || k % 64)
+        throw std::invalid_argument("checksummed_gemm: this kernel needs stride 8, M % 128 == 0, "
+                                    "W % 256 == 0, K % 64 == 0");
+    if (c_init && !cp_init) throw std::invalid_argument("checksummed_gemm: c_init without cp_init");
+    if (c_init && (c_init->rows() != m || c_init->cols() != w || cp_init->c1.rows() != m))
+        throw std::invalid_argument("checksummed_gemm: c_init shape mismatch");
+    // operands to the fp16 grid: X = a [M x K], W = bt^T [W x K] (the kernel's nn.Linear layout)
+    std::vector<uint16_t> hx(static_cast<size_t>(m) * k), hw(static_cast<size_t>(w) * k);
+    for (size_t i = 0; i < hx.size(); ++i) hx[i] = to_half_bits(a.data()[i]);
+    for (int r = 0; r < k; ++r)
+        for (int c = 0; c < w; ++c) hw[static_cast<size_t>(c) * k + r] = to_half_bits(bt(r, c));
+    efta_gemm_desc d{m, w, k, 8, 256, std::numeric_limits<double>::infinity(), 0};
+    const int tiles = w / 256;
+    const size_t ny = static_cast<size_t>(m) * w, ncs = static_cast<size_t>(m) * tiles * 16, nc = m * 8ull;
+    DevBuf dx(hx.size() * 2), dw(hw.size() * 2), dwc(efta_abft_weight_cs_bytes(&d)), dy(ny * 4), dcs(ncs * 4),
+        dcnt(sizeof(efta_counters)), d1(nc * 4), d2(nc * 4), di(c_init ? ny * 4 : 0), di1(c_init ? nc * 4 : 0),
+        di2(c_init ? nc * 4 : 0);
+    cuda_check(cudaMemcpy(dx.p, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice));
+    cuda_check(cudaMemcpy(dw.p, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice));
+    capi_check(efta_abft_encode_weight_f16(&d, dw.as<uint16_t>(), dwc.as<uint16_t>(), nullptr));
+    capi_check(efta_abft_gemm_ex(&d, dx.as<uint16_t>(), dw.as<uint16_t>(), dwc.as<uint16_t>(), dy.p, 1,
+                                 dcs.as<float>(), nullptr, 0, nullptr, 0, dcnt.as<efta_counters>(), nullptr));
+    if (c_init) {
+        cuda_check(cudaMemcpy(di.p, c_init->data(), ny * 4, cudaMemcpyHostToDevice));
+        cuda_check(cudaMemcpy(di1.p, cp_init->c1.data(), nc * 4, cudaMemcpyHostToDevice));
+        cuda_check(cudaMemcpy(di2.p, cp_init->c2.data(), nc * 4, cudaMemcpyHostToDevice));
+        add_into<<<static_cast<unsigned>((ny + 255) / 256), 256>>>(ny, di.as<float>(), dy.as<float>());
+    }
+    compose_tile_checksums<<<static_cast<unsigned>((nc + 255) / 256), 256>>>(
+        m, tiles, dcs.as<float>(), c_init ? di1.as<float>() : nullptr, c_init ? di2.as<float>() : nullptr,
+        d1.as<float>(), d2.as<float>());
+    cuda_check(cudaGetLastError());
+    Matrix c(m, w);
+    ChecksumPair cp;
+    cp.stride = stride;
+    cp.groups = w / stride;
+    cp.c1 = Matrix(m, stride);
+    cp.c2 = Matrix(m, stride);
+    cuda_check(cudaMemcpy(c.data(), dy.p, ny * 4, cudaMemcpyDeviceToHost));
+    cuda_check(cudaMemcpy(cp.c1.data(), d1.p, nc * 4, cudaMemcpyDeviceToHost));
+    cuda_check(cudaMemcpy(cp.c2.data(), d2.p, nc * 4, cudaMemcpyDeviceToHost));
+    return {std::move(c), std::move(cp)};
+}
+
+// ------------------------------------------------------------------ calibration / sweep
+namespace {
+struct Family {
+    double exp = -std::numeric_limits<double>::infinity(), out = -std::numeric_limits<double>::infinity(),
+           lin = -std::numeric_limits<double>::infinity();
+    bool hard = false;
+};
+// FamilyResiduals (src/campaign.cpp:55-85) of one observation run: the device keeps the worst
+// clean residual per family (family_max) and logs range events, which are the "hard" trips
+Family family_of(const FTReport& rep) {
+    Family f;
+    if (rep.family_max[0] > 0) f.exp = rep.family_max[0];
+    if (rep.family_max[1] > 0) f.out = rep.family_max[1];
+    if (rep.family_max[2] > 0) f.lin = rep.family_max[2];
+    for (const auto& e : rep.events) {
+        if (e.kind == CheckKind::FACTOR_RANGE || e.kind == CheckKind::ROWSUM_RANGE) f.hard = true;
+        const double r = e.rep.residual;
+        if (!std::isfinite(r)) continue;
+        if (e.kind == CheckKind::EXP_CHECKSUM) f.exp = std::max(f.exp, r);
+        if (e.kind == CheckKind::OUTPUT_CHECKSUM) f.out = std::max(f.out, r);
+        if (e.kind == CheckKind::SCORE_CHECKSUM) f.lin = std::max(f.lin, r);
+    }
+    return f;
+}
+}  // namespace
+
+CalibrationResult calibrate_thresholds(const AttnConfig& cfg_in, FTMode mode, int trials, double safety,
+                                       uint64_t seed) {
+    AttnConfig cfg = cfg_in;
+    cfg.validate();
+    if (trials <= 0) throw ConfigError("calibration: trials must be positive");
+    if (safety < 1.0) throw ConfigError("calibration: safety factor must be >= 1");
+    const double inf = std::numeric_limits<double>::infinity();
+    KernelKnobs knobs;
+    knobs.observe_linear = true;
+    double mexp = -inf, mout = -inf, mlin = -inf;
+    for (int t = 0; t < trials; ++t) {
+        Rng rng(trial_seed(seed, static_cast<uint64_t>(t)));
+        const Matrix q = random_half_matrix(cfg.seq_len, cfg.head_dim, rng);
+        const Matrix k = random_half_matrix(cfg.seq_len, cfg.head_dim, rng);
+        const Matrix v = random_half_matrix(cfg.seq_len, cfg.head_dim, rng);
+        auto res = efta_forward(q, k, v, cfg, Thresholds::observe(), mode, nullptr, &knobs);
+        const Family f = family_of(res.second);
+        mexp = std::max(mexp, f.exp);
+        mout = std::max(mout, f.out);
+        mlin = std::max(mlin, f.lin);
+    }
+    CalibrationResult r;
+    r.max_exp = std::isfinite(mexp) ? mexp : 0.0;
+    r.max_out = std::isfinite(mout) ? mout : 0.0;
+    r.max_lin = std::isfinite(mlin) ? mlin : 0.0;
+    r.degenerate = !(std::isfinite(mexp) && mexp > 0.0) || !(std::isfinite(mout) && mout > 0.0) ||
+                   !(std::isfinite(mlin) && mlin > 0.0);
+    r.thr.eps1 = std::isfinite(mexp) ? mexp * safety : inf;
+    r.thr.eps2 = std::isfinite(mout) ? mout * safety : inf;
+    r.thr.eps_lin = std::isfinite(mlin) ? mlin * safety : inf;
+    return r;
+}
+
+std::vector<SweepPoint> threshold_sweep(const AttnConfig& cfg_in, FTMode mode, const Thresholds& base, int trials,
+                                        uint64_t seed, int points) {
+    AttnConfig cfg = cfg_in;
+    cfg.validate();
+    if (trials <= 0 || points <= 1) throw ConfigError("sweep: trials and points must be positive");
+    KernelKnobs knobs;
+    knobs.observe_linear = true;
+    const std::vector<FaultSite> sites = {FaultSite::GEMM1_OUT,  FaultSite::SUB_MAX,        FaultSite::EXP_OUT,
+                                          FaultSite::REDUCE_MAX, FaultSite::REDUCE_SUM,     FaultSite::RESCALE_FACTOR,
+                                          FaultSite::GEMM2_ACC,  FaultSite::NORMALIZE_OUT};
+    std::vector<Family> clean_runs, fault_runs;
+    for (int t = 0; t < trials; ++t) {
+        Rng rng(trial_seed(seed, static_cast<uint64_t>(t)));
+        const Matrix q = random_half_matrix(cfg.seq_len, cfg.head_dim, rng);
+        const Matrix k = random_half_matrix(cfg.seq_len, cfg.head_dim, rng);
+        const Matrix v = random_half_matrix(cfg.seq_len, cfg.head_dim, rng);
+        clean_runs.push_back(family_of(efta_forward(q, k, v, cfg, Thresholds::observe(), mode, nullptr, &knobs).second));
+        FaultInjector inj(sample_random_plan(cfg, sites, rng));
+        fault_runs.push_back(family_of(efta_forward(q, k, v, cfg, Thresholds::observe(), mode, &inj, &knobs).second));
+    }
+    auto trips = [&](const Family& f, double mult) {
+        if (f.hard) return true;
+        if (std::isfinite(f.exp) && std::isfinite(base.eps1) && f.exp > base.eps1 * mult) return true;
+        if (std::isfinite(f.out) && std::isfinite(base.eps2) && f.out > base.eps2 * mult) return true;
+        if (std::isfinite(f.lin) && std::isfinite(base.eps_lin) && f.lin > base.eps_lin * mult) return true;
+        return false;
+    };
+    std::vector<SweepPoint> sweep;
+    for (int p = 0; p < points; ++p) {
+        SweepPoint sp;
+        sp.multiplier = std::pow(10.0, -2.0 + 4.0 * p / (points - 1));
+        int det = 0, fa = 0;
+        for (const auto& f : fault_runs) det += trips(f, sp.multiplier) ? 1 : 0;
+        for (const auto& f : clean_runs) fa += trips(f, sp.multiplier) ? 1 : 0;
+        sp.detection_rate = static_cast<double>(det) / trials;
+        sp.false_alarm_rate = static_cast<double>(fa) / trials;
+        sweep.push_back(sp);
+    }
+    return sweep;
 }
 
 const char* outcome_name(Outcome o) {

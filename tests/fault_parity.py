@@ -15,10 +15,11 @@ Contract:
         the upset moved (> 1.5x the fault-free twin's residual of the same check);
       - lin_margin: a GEMM1_OUT upset with eps_lin/4 < |after - before| < 4 eps_lin (the
         linear repair of the score tile decides between locating the cell and recomputing);
-      - range_row: a range-restricted denominator (REDUCE_SUM) where both sides agree on the
-        outcome and on every event but the located cell of the final output check: the row is
-        rescaled by l/lower-bound and checked at eps2 * N / l, so its violated groups sit at the
-        noise floor and the "largest correction" cell is picked by rounding.
+      - denominator_row: a corrupted or range-restricted denominator (REDUCE_SUM upset, or any
+        range replacement) where both sides agree on the outcome and on every event but the
+        located cell of the final output check: the row is divided by a wrong l, which scales its
+        noise-level group residuals past eps2, so which cell gets the "largest correction" is
+        picked by rounding.
     The marginal band (near_threshold or lin_margin, mismatched or not) is reported.
 """
 from __future__ import annotations
@@ -169,11 +170,11 @@ def run_parity(plans, seq, d, thr):
         same = o["fired"] == g["fired"] and o["outcome"] == g["outcome"] and o["events"] == g_ev
         lin = t[0] == 0 and 0.25 * thr.eps_lin < o["delta"] < 4.0 * thr.eps_lin
         strip = lambda ev: [e[:4] if e[0] == "output_checksum" else e for e in ev]  # noqa: E731
-        range_row = ((o["range_replacements"] > 0 or g["range_replacements"] > 0) and
+        range_row = ((t[0] == 4 or o["range_replacements"] > 0 or g["range_replacements"] > 0) and
                      o["fired"] == g["fired"] and o["outcome"] == g["outcome"] and
                      strip(o["events"]) == strip(g_ev))
         why = [] if same else [w for w, ok in (("near_threshold", o["near"]), ("lin_margin", lin),
-                                                ("range_row", range_row)) if ok]
+                                                ("denominator_row", range_row)) if ok]
         rows.append(dict(spec=":".join([SITES[t[0]]] + [str(x) for x in t[1:6]]), site=SITES[t[0]], bit=t[5],
                          seed=seed, oracle=o["outcome"], gpu=g["outcome"], fired_o=o["fired"],
                          fired_g=g["fired"], ev_o=o["events"], ev_g=g_ev, same=same, explained=why,
