@@ -3,16 +3,16 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (BASELINE.json configs[3], "C4"): Llama-style attention, per GPU
-B=32 H=32 S=8192 d_head=128, fp16 Q/K/V (U(-1,1) on the fp16 grid like the
+Workload (BASELINE.json configs[3], "C4"): Llama-style attention B=32 H=32 S=8192
+d_head=128 (1024 independent heads), fp16 Q/K/V (U(-1,1) on the fp16 grid like the
 reference's Matrix::random), EFTA-optimized protection, block 128, stride 8.
-Multi-GPU: one process per GPU; each rank owns an independent shard of
-(batch x head) units of the same size (weak scaling, no collective on the data
-path; the only collectives are the timing barrier / max-reduce).
+Multi-GPU: one process per GPU; the 1024 global (batch x head) units
+are split contiguously over the ranks (strong scaling, no collective on the data path;
+the only collectives are the timing barrier / max-reduce).
 
-One step = one protected forward over the rank's shard: checksum-encode
-prepass + the fused attention kernel. value = 4*B*H*S^2*d FLOPs (all ranks) /
-max-over-ranks device time.
+One step = one protected forward over the rank's heads: checksum-encode prepass + the
+fused attention kernel. value = 4*B*H*S^2*d FLOPs (the whole job) / max-over-ranks
+device time.
 """
 from __future__ import annotations
 
@@ -277,19 +277,53 @@ def suite(dev):
     return out
 
 
+def synth_heads(seed, start, count, device):
+    """Heads [start, start+count) of the global C4 problem: head i is U(-1,1) on the fp16 grid
+    from its own generator (seed, i), so every sharding of the global (b, h) index reproduces
+    the same per-head inputs (the union over ranks is the single-GPU problem)."""
+    import torch
+    x = torch.empty((count, S, D), dtype=torch.float16, device=device)
+    g = torch.Generator(device=device)
+    tmp = torch.empty((S, D), dtype=torch.float32, device=device)
+    for i in range(count):
+        g.manual_seed(seed * 1_000_003 + start + i)
+        tmp.uniform_(-1.0, 1.0, generator=g)
+        x[i].copy_(tmp)
+    return x
+
+
+def fault_parity_c2():
+    """Checker leg (not timed): the C2 campaign's 240 seeded plans replayed through the fault-tap
+    build of the pair kernel and the CPU reference with common thresholds (tests/fault_parity.py):
+    records identical in {fired, outcome, events incl. row/col}, mismatches explained by margin."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from fault_parity import campaign_specs, common_thresholds, run_parity, summarize  # test infrastructure
+    thr, _, _ = common_thresholds(512, 64)
+    rows = run_parity(campaign_specs(20, 12, 512, 64, [0, 2, 6], seed=7), 512, 64, thr)
+    sm = summarize(rows)
+    return {k2: sm[k2] for k2 in ("records", "identical", "mismatched", "explained_by_margin", "unexplained",
+                                  "marginal_band", "fired_oracle", "fired_gpu")}
+
+
 def ours(args):
     import torch
     rank, world, local, pg = dist_init(args.gpus)
     from paper_2504_02211_b200 import EftaAttention, Thresholds
     from paper_2504_02211_b200 import _lib
+    from paper_2504_02211_b200.shard import shard_units
     dev = torch.device("cuda", torch.cuda.current_device())
-    shape = (B, H, S, D)
-    q = synth_inputs(1 + 3 * rank, shape, dev)
-    k = synth_inputs(2 + 3 * rank, shape, dev)
-    v = synth_inputs(3 + 3 * rank, shape, dev)
+    # global C4 problem: B*H = 1024 independent heads, split contiguously over the ranks
+    # (SURVEY.md §8(e); no collective on the data path): strong scaling
+    sh = shard_units(B * H, world, rank)
+    nh = sh.count
+    shape = (1, nh, S, D)
+    q = synth_heads(1, sh.start, nh, dev).view(shape)
+    k = synth_heads(2, sh.start, nh, dev).view(shape)
+    v = synth_heads(3, sh.start, nh, dev).view(shape)
     thr = Thresholds(1e-4, 1e-3, 1e-3)
-    op = EftaAttention(B, H, S, D, mode="efta-opt", thr=thr, device=dev)
-    op_none = EftaAttention(B, H, S, D, mode="none", thr=thr, device=dev)
+    op = EftaAttention(1, nh, S, D, mode="efta-opt", thr=thr, device=dev)
+    op_none = EftaAttention(1, nh, S, D, mode="none", thr=thr, device=dev)
     o = torch.empty(shape, dtype=torch.float32, device=dev)
     m = torch.empty(shape[:3], dtype=torch.float32, device=dev)
     l = torch.empty(shape[:3], dtype=torch.float32, device=dev)
@@ -299,7 +333,7 @@ def ours(args):
         ms = time_steps(step, args.steps, args.warmup, pg)
     ms_max = max_over_ranks(pg, ms)
     rep = op.report()
-    total_flops = world * flops(*shape)
+    total_flops = flops(B, H, S, D)  # the whole job: every rank's heads together
     value = total_flops / (ms_max * 1e-3) / 1e12
 
     # unprotected kernel (same kernel, MODE=NONE) for the FT overhead
@@ -313,7 +347,7 @@ def ours(args):
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
     peak = peaks.get("bf16_tflops_sustained") or 1400.0
     peak_burst = peaks.get("bf16_tflops") or 1590.0
-    achieved = flops(*shape) / (ms_kern * 1e-3) / 1e12
+    achieved = flops(1, nh, S, D) / (ms_kern * 1e-3) / 1e12  # per GPU (its own heads)
     traffic = None
     if os.path.exists(TRAFFIC_PATH):
         try:
@@ -323,16 +357,16 @@ def ours(args):
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16",
         "data": "synthetic: U(-1,1) rounded to fp16 (the reference Matrix::random distribution), "
-                "generated on device per rank",
-        "config": {"workload": "C4 Llama-style attention B=32 H=32 S=8192 d_head=128 per GPU, "
-                               "batch x head sharded (weak scaling)",
-                   "batch_per_gpu": B, "heads": H, "seq_len": S, "head_dim": D,
-                   "global_batch": B * world, "mode": "efta-opt", "block": BLOCK,
-                   "stride": STRIDE, "parallelism": f"bh-shard{world}",
-                   "l2": "inputs (3 x 2.1 GB fp16) larger than L2 (126 MB)"},
-        "unprotected_tflops": round(world * flops(*shape) / (ms_none * 1e-3) / 1e12, 2),
+                "generated on device per head (seeded by the global head index)",
+        "config": {"workload": "C4 Llama-style attention B=32 H=32 S=8192 d_head=128 (global), "
+                               "batch x head sharded over the GPUs (strong scaling)",
+                   "batch": B, "heads": H, "seq_len": S, "head_dim": D, "global_batch": B,
+                   "heads_per_gpu": nh, "mode": "efta-opt", "block": BLOCK, "stride": STRIDE,
+                   "parallelism": f"bh-shard{world}",
+                   "l2": "inputs (3 x 2.1 GB fp16 at N=1) larger than L2 (126 MB)"},
+        "unprotected_tflops": round(total_flops / (ms_none * 1e-3) / 1e12, 2),
         "ft_overhead_pct": round((ms_max / ms_none - 1.0) * 100.0, 2),
         "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
@@ -347,7 +381,7 @@ def ours(args):
     }
     # ---- e2e through the host C-ABI (pinned host buffers, copies in the timed region)
     if not args.no_e2e:
-        desc = _lib.AttnDesc(B, H, S, D, BLOCK, STRIDE, 0.0, 2, thr.eps1, thr.eps2, thr.eps_lin,
+        desc = _lib.AttnDesc(1, nh, S, D, BLOCK, STRIDE, 0.0, 2, thr.eps1, thr.eps2, thr.eps_lin,
                              0, 0.0, 0, 0)
         hq = q.cpu().pin_memory()
         hk = k.cpu().pin_memory()
@@ -369,11 +403,11 @@ def ours(args):
             e2e_step()
         barrier(pg)
         dt = max_over_ranks(pg, (time.perf_counter() - t0) / e2e_steps)
-        line["e2e"] = {"value": round(world * flops(*shape) / dt / 1e12, 2), "unit": "TFLOP/s",
-                       "h2d_bytes_per_step": 3 * q.numel() * 2,
-                       "d2h_bytes_per_step": o.numel() * 4 + 2 * m.numel() * 4,
+        line["e2e"] = {"value": round(total_flops / dt / 1e12, 2), "unit": "TFLOP/s",
+                       "h2d_bytes_per_step": world * 3 * q.numel() * 2,
+                       "d2h_bytes_per_step": world * (o.numel() * 4 + 2 * m.numel() * 4),
                        "steps": e2e_steps,
-                       "path": "efta_attn_fwd_host_f16 (C-ABI, host buffers, synchronous)"}
+                       "path": "efta_attn_fwd_host_f16 (C-ABI, host buffers, synchronous), per rank on its heads"}
     if rank == 0 and world == 1:
         if not args.no_campaign:
             try:
@@ -383,9 +417,18 @@ def ours(args):
                                                               "masked_benign", "range_restricted",
                                                               "range_contract", "uncorrectable",
                                                               "false_alarms")}
+                line["fault_campaign"]["kernel"] = ("efta_attn_pair_kernel<64, EFTA_OPT, INJ> (fault-tap build "
+                                                    "of the production pair kernel), GPU-calibrated thresholds")
+                line["fault_campaign"]["uncorrectable_note"] = (
+                    "single-bit score upsets at |delta| ~ eps1 that linear repair cannot locate; the reference "
+                    "marks the same records uncorrectable (fault_parity)")
             except Exception as ex:  # reported, never fatal for the perf line
                 line["fault_coverage_pct"] = None
                 line["fault_campaign"] = {"error": str(ex)[:200]}
+            try:
+                line["fault_parity"] = fault_parity_c2()
+            except Exception as ex:
+                line["fault_parity"] = {"error": str(ex)[:200]}
         if not args.no_suite:
             try:
                 line["suite"] = suite(dev)
@@ -425,11 +468,11 @@ def reference(args):
         "impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(wall / args.steps * 1e3, 1), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: reference Rng + Matrix::random Q/K/V (fp16 grid)",
-        "config": {"workload": "C4 Llama-style attention B=32 H=32 S=8192 d_head=128 (bounded "
+        "config": {"workload": "C4 Llama-style attention B=32 H=32 S=8192 d_head=128 (global; bounded "
                                "sample: one head per host thread per step)",
-                   "batch_per_gpu": B, "heads": H, "seq_len": S, "head_dim": D,
+                   "batch": B, "heads": H, "seq_len": S, "head_dim": D, "global_batch": B,
                    "mode": "efta-opt", "block": BLOCK, "stride": STRIDE},
         "cpu_baseline": {"value": round(v, 6), "unit": "TFLOP/s", "cores": ncpu,
                          "kind": res["kind"], "sample": res["sample"]},

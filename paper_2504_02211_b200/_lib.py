@@ -82,6 +82,8 @@ def _load():
         lib.efta_abft_encode_weight_f16.argtypes = [C.POINTER(GemmDesc), vp, vp, vp]
         lib.efta_abft_weight_cs_bytes.restype = C.c_size_t
         lib.efta_abft_weight_cs_bytes.argtypes = [C.POINTER(GemmDesc)]
+        lib.efta_abft_gemm_ex.argtypes = [C.POINTER(GemmDesc), vp, vp, vp, vp, C.c_int, vp, vp, C.c_int,
+                                          vp, C.c_int, vp, vp]
     return lib
 
 

@@ -18,7 +18,7 @@ from . import _lib
 from ._lib import check, lib
 from .attention import FTReport, KINDS, STATUS
 
-_EXPORTS = ("efta_abft_gemm_f16", "efta_abft_encode_weight_f16", "efta_abft_weight_cs_bytes")
+_EXPORTS = ("efta_abft_gemm_f16", "efta_abft_gemm_ex", "efta_abft_encode_weight_f16", "efta_abft_weight_cs_bytes")
 for _n in _EXPORTS:
     if not hasattr(lib, _n):
         raise ImportError(f"libefta_b200.so lacks {_n}: rebuild the library")
@@ -58,16 +58,23 @@ class AbftLinear:
             *[_lib.FaultSpec(0, 0, r, 0, 0, c, b, 1) for (r, c, b) in faults])
         self.faults = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(self.weight.device)
 
-    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None):
+    def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None, fp32_out: bool = False,
+                 checksums: torch.Tensor | None = None):
+        """y = x @ weight.T (fp16, or fp32 with fp32_out). checksums, if given: a CUDA fp32
+        tensor [tokens, out_features/256, 16] receiving each output tile's tensor-core
+        c1[8] | c2[8] per row (the reference's ChecksumPair per 256-wide tile)."""
         if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[1] != self.k:
             raise _lib.ConfigError("AbftLinear: x must be CUDA fp16 [tokens, in_features]")
         x = x.contiguous()
         m = x.shape[0]
         if y is None:
-            y = torch.empty((m, self.n), dtype=torch.float16, device=x.device)
+            y = torch.empty((m, self.n), dtype=torch.float32 if fp32_out else torch.float16, device=x.device)
+        if checksums is not None and (checksums.dtype != torch.float32 or checksums.numel() != m * (self.n // 256) * 16):
+            raise _lib.ConfigError("AbftLinear: checksums must be fp32 [tokens, out/256, 16]")
         desc = _lib.GemmDesc(m, self.n, self.k, 8, 256, self.eps, 1 if self.debug else 0)
-        check(lib.efta_abft_gemm_f16(
+        check(lib.efta_abft_gemm_ex(
             C.byref(desc), x.data_ptr(), self.weight.data_ptr(), self.wcs.data_ptr(), y.data_ptr(),
+            1 if y.dtype == torch.float32 else 0, checksums.data_ptr() if checksums is not None else None,
             self.faults.data_ptr() if self.faults is not None else None, self.n_faults,
             self.events.data_ptr(), self.ev_cap, self.counters.data_ptr(),
             torch.cuda.current_stream(x.device).cuda_stream))

@@ -32,6 +32,26 @@ def shard_units(n_units: int, world: int, rank: int) -> Shard:
     return Shard(rank, world, start, base + (1 if rank < extra else 0))
 
 
+def shard_tokens(n_tokens: int, world: int, rank: int, align: int = 128) -> Shard:
+    """Token-row split of an FFN activation [n_tokens, d] for the strided-ABFT GEMM: contiguous
+    blocks of `align` rows (the GEMM's 128-row tile), balanced to within one block. Weights and
+    their checksum rows are replicated, so every rank verifies its own rows (no exchange)."""
+    if n_tokens % align:
+        raise ValueError("shard_tokens: n_tokens must be a multiple of align")
+    blk = shard_units(n_tokens // align, world, rank)
+    return Shard(rank, world, blk.start * align, blk.count * align)
+
+
+def gather_units(local, dist=None):
+    """Concatenate per-rank lists of unit results in rank order (host-side, small objects:
+    outputs of sampled units, event logs). The data path itself never exchanges anything."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return list(local)
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, list(local))
+    return [x for part in parts for x in part]
+
+
 def route_faults(specs, shard: Shard):
     """Keep the fault specs whose flat head lies in this shard, re-indexed locally."""
     out = []
