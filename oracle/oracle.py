@@ -18,8 +18,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 SITES = ["GEMM1_OUT", "SUB_MAX", "EXP_OUT", "REDUCE_MAX", "REDUCE_SUM",
          "RESCALE_FACTOR", "GEMM2_ACC", "NORMALIZE_OUT"]
-MODES = {"none": 0, "efta": 1, "efta-opt": 2}
-KINDS = ["score_checksum", "exp_checksum", "factor_range", "rowsum_range", "output_checksum"]
+MODES = {"none": 0, "efta": 1, "efta-opt": 2, "decoupled": 3}  # decoupled: the reference (_ref) only
+KINDS = ["score_checksum", "exp_checksum", "factor_range", "rowsum_range", "output_checksum",
+         "dmr_softmax", "block_checksum"]
 STATUS = ["clean", "corrected", "detected_uncorrectable", "nonfinite"]
 
 
@@ -195,7 +196,7 @@ class Oracle:
         n, d = q.shape
         nb = n // block if block > 0 else 0
         if ev_cap is None:
-            ev_cap = max(64, 4 * nb * (nb + 2) + 16)
+            ev_cap = max(64, 4 * nb * (nb + 2) + 16) + (4 * n if mode == "decoupled" else 0)
         o = np.zeros((n, d), np.float32)
         m = np.zeros(n, np.float32)
         l = np.zeros(n, np.float32)

@@ -6,6 +6,8 @@
 // copied into this repository; this file only calls the reference's public
 // functions:
 //   efta_forward            include/efta/efta.hpp:86-89
+//   decoupled_ft_forward    include/efta/efta.hpp:94-96 (mode 3 = FTMode::DECOUPLED, dispatched
+//                           like the campaign's forward(), src/campaign.cpp:18-23)
 //   standard_attention      include/efta/attention.hpp:19-21
 //   encode_strided          include/efta/abft.hpp:38
 //   checksummed_gemm        include/efta/abft.hpp:73-77
@@ -126,8 +128,10 @@ int eref_efta_forward(int n, int d, int block, int stride, float scale, int mode
         KernelKnobs knobs;
         knobs.observe_linear = observe_linear != 0;
         knobs.rowmax_bias = rowmax_bias;
-        auto [out, rep] = efta_forward(mq, mk, mv, cfg, thr, static_cast<FTMode>(mode),
-                                       n_specs > 0 ? &inj : nullptr, &knobs);
+        auto [out, rep] = static_cast<FTMode>(mode) == FTMode::DECOUPLED
+                              ? decoupled_ft_forward(mq, mk, mv, cfg, thr, n_specs > 0 ? &inj : nullptr, &knobs)
+                              : efta_forward(mq, mk, mv, cfg, thr, static_cast<FTMode>(mode),
+                                             n_specs > 0 ? &inj : nullptr, &knobs);
         to_ptr(out, o);
         if (m_out) std::memcpy(m_out, rep.final_m.data(), sizeof(float) * n);
         if (l_out) std::memcpy(l_out, rep.final_l.data(), sizeof(float) * n);

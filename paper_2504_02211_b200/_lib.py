@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("EFTA_LIB") or os.path.join(PKG, "libefta_b200.so")
 
 SITES = ["GEMM1_OUT", "SUB_MAX", "EXP_OUT", "REDUCE_MAX", "REDUCE_SUM",
          "RESCALE_FACTOR", "GEMM2_ACC", "NORMALIZE_OUT"]
-MODES = {"none": 0, "efta": 1, "efta-opt": 2, "efta_optimized": 2}
+MODES = {"none": 0, "efta": 1, "efta-opt": 2, "efta_optimized": 2, "decoupled": 3}
 KINDS = ["score_checksum", "exp_checksum", "factor_range", "rowsum_range", "output_checksum",
          "dmr_softmax", "block_checksum"]
 STATUS = ["clean", "corrected", "detected_uncorrectable", "nonfinite"]

@@ -34,6 +34,7 @@ UNITS = [
     ("abft_gemm.cu", []),
     ("abft_verify.cu", []),
     ("efta_host.cu", []),
+    ("decoupled.cu", []),
 ]
 
 
@@ -81,7 +82,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(units)) as ex:
         futs = [ex.submit(_compile, s, d, _obj(s, d) + ".log", force) for s, d in units]
         objs = [f.result() for f in futs]
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcuda"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcuda", "-lcublas",
+           "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

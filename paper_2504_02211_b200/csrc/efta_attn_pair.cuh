@@ -89,6 +89,16 @@ __device__ __forceinline__ void mbar_arrive_rel_cluster(uint64_t* bar, uint32_t 
         "r"(cta)
         : "memory");
 }
+// consumer release of a tile-ring slot: relaxed (a release at cluster scope costs a GPU-scope
+// MEMBAR + ERRBAR per warp and tile; the slot's value is already in a register, and the
+// producer rewrites the slot only kTileRing tiles later)
+__device__ __forceinline__ void mbar_arrive_relaxed_cluster(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
     uint32_t ok = 0;
     while (!ok) {
@@ -108,7 +118,7 @@ __device__ __forceinline__ int pair_next_tile(const int* tinfo, uint64_t* tfull,
     mbar_wait_acq_cluster(&tfull[slot], static_cast<uint32_t>(k / kTileRing) & 1u);
     const int u = *reinterpret_cast<const volatile int*>(&tinfo[slot]);
     if (warp_wide) __syncwarp();
-    if (!warp_wide || (threadIdx.x & 31) == 0) mbar_arrive_rel_cluster(&tempty[slot], 0);
+    if (!warp_wide || (threadIdx.x & 31) == 0) mbar_arrive_relaxed_cluster(&tempty[slot], 0);
     return u;
 }
 

@@ -18,6 +18,12 @@
 #include "efta_launch.h"
 #include "efta_encode.cuh"
 
+namespace efta_dec {  // csrc/decoupled.cu
+size_t workspace_bytes(int bh, int N, int D);
+std::string forward(const efta_sm100::AttnParams& base, int bh, int N, int D, const __half* q, const __half* k,
+                    const __half* v, float* o, void* ws, cudaStream_t st);
+}
+
 using namespace efta_sm100;
 
 namespace {
@@ -83,8 +89,7 @@ int validate(const efta_attn_desc* d) {
     if (d->block != kBlock) return fail(1, "efta_b200: block must be 128 (tcgen05 M=128 tile)");
     if (d->stride != kStride) return fail(1, "efta_b200: stride must be 8");
     if (d->head_dim != 64 && d->head_dim != 128) return fail(1, "efta_b200: head_dim must be 64 or 128");
-    if (d->mode < EFTA_MODE_NONE || d->mode > EFTA_MODE_EFTA_OPT)
-        return fail(1, "efta_b200: unsupported mode (DECOUPLED is not provided)");
+    if (d->mode < EFTA_MODE_NONE || d->mode > EFTA_MODE_DECOUPLED) return fail(1, "efta_b200: unsupported mode");
     const long long bh = static_cast<long long>(d->batch) * d->heads;
     if (bh > 65535) return fail(1, "efta_b200: batch*heads must be <= 65535");
     return 0;
@@ -107,7 +112,11 @@ WsLayout ws_layout(const efta_attn_desc* d) {
     w.total = w.scratch + 256;  // scratch: the persistent pair kernel's tile counter
     return w;
 }
-size_t ws_bytes(const efta_attn_desc* d) { return ws_layout(d).total; }
+size_t ws_bytes(const efta_attn_desc* d) {
+    if (d->mode == EFTA_MODE_DECOUPLED)
+        return efta_dec::workspace_bytes(d->batch * d->heads, d->seq_len, d->head_dim);
+    return ws_layout(d).total;
+}
 
 // Unprotected / EFTA-optimized calls run on CTA pairs (cta_group::2) whenever the number of
 // query tiles is even; the `debug` (fault-tap / observation) calls of EFTA_OPT run the tap
@@ -182,6 +191,36 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
         return fail(1, "efta_attn_fwd_f16: fault injection needs the debug (tap) kernel variant");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int bh = d->batch * d->heads, nblk = d->seq_len / kBlock, D = d->head_dim;
+    if (d->mode == EFTA_MODE_DECOUPLED) {
+        // the decoupled baseline (src/decoupled.cpp:98-282): three kernels + cuBLAS GEMMs with
+        // the N^2 intermediates in the workspace (csrc/decoupled.cu)
+        if (workspace == nullptr || workspace_bytes < ws_bytes(d))
+            return fail(1, "efta_attn_fwd_f16: workspace too small");
+        CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(efta_counters), st));
+        AttnParams p{};
+        p.seq_len = d->seq_len;
+        p.nblk = nblk;
+        p.n_heads_flat = bh;
+        p.scale = d->scale == 0.0f ? 1.0f / std::sqrt(static_cast<float>(D)) : d->scale;
+        p.rowmax_bias = d->rowmax_bias;
+        p.eps1 = d->eps1;
+        p.eps2 = d->eps2;
+        p.eps_lin = d->eps_lin;
+        p.m_out = m_out;
+        p.l_out = l_out;
+        p.events = events;
+        p.ev_cap = events ? ev_cap : 0;
+        p.counters = counters;
+        p.faults = faults;
+        p.n_faults = faults ? n_faults : 0;
+        p.fired = fired;
+        p.fired_cap = fired ? fired_cap : 0;
+        const std::string err = efta_dec::forward(p, bh, d->seq_len, D, reinterpret_cast<const __half*>(q),
+                                                  reinterpret_cast<const __half*>(k),
+                                                  reinterpret_cast<const __half*>(v), o, workspace, st);
+        if (!err.empty()) return fail(2, err);
+        return 0;
+    }
     const bool prot = d->mode != EFTA_MODE_NONE;
     const bool pair = use_pair(d);
     if ((prot || pair) && (workspace == nullptr || workspace_bytes < ws_bytes(d)))

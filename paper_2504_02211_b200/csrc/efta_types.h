@@ -13,8 +13,9 @@ enum efta_site {
     EFTA_GEMM1_OUT = 0, EFTA_SUB_MAX, EFTA_EXP_OUT, EFTA_REDUCE_MAX, EFTA_REDUCE_SUM,
     EFTA_RESCALE_FACTOR, EFTA_GEMM2_ACC, EFTA_NORMALIZE_OUT, EFTA_SITE_COUNT
 };
-/* FTMode order == reference include/efta/efta.hpp:24 (DECOUPLED not provided) */
-enum efta_mode { EFTA_MODE_NONE = 0, EFTA_MODE_EFTA = 1, EFTA_MODE_EFTA_OPT = 2 };
+/* FTMode order == reference include/efta/efta.hpp:24 (DECOUPLED: the three-kernel baseline,
+ * src/decoupled.cpp:98-282, csrc/decoupled.cu) */
+enum efta_mode { EFTA_MODE_NONE = 0, EFTA_MODE_EFTA = 1, EFTA_MODE_EFTA_OPT = 2, EFTA_MODE_DECOUPLED = 3 };
 /* CheckKind order == reference include/efta/efta.hpp:30-38 */
 enum efta_check {
     EFTA_SCORE_CHECKSUM = 0, EFTA_EXP_CHECKSUM, EFTA_FACTOR_RANGE, EFTA_ROWSUM_RANGE,

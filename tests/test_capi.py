@@ -46,13 +46,16 @@ def _desc(**kw):
     (dict(block=96, seq_len=480), False, "stride must divide block"),  # 96 % 8 == 0 -> geometry
     (dict(head_dim=60), False, "stride must divide head_dim"),  # config.hpp:37-38
     (dict(head_dim=96), False, "head_dim must be 64 or 128"),
-    (dict(mode=3), False, "DECOUPLED"),
+    (dict(mode=3), True, ""),                                  # DECOUPLED baseline (csrc/decoupled.cu)
+    (dict(mode=4), False, "unsupported mode"),
 ])
 def test_validate_mirrors_attnconfig(kw, ok, msg):
     from paper_2504_02211_b200 import _lib
     d = _desc(**kw)
     rc = _lib.lib.efta_attn_validate(C.byref(d))
     assert (rc == 0) == ok
+    if ok:
+        assert _lib.lib.efta_attn_workspace_bytes(C.byref(d)) > 0
     if not ok:
         assert rc == 1
         err = _lib.last_error()
@@ -130,3 +133,16 @@ def test_classify_trial_ladder():  # test_campaign.cpp:190-254
     out = ref.copy(); out[5] *= 1.2
     assert classify(out, ref, 0, 0, False, l_ok, FaultSpec.parse("REDUCE_SUM:0:0:5:0:3"),
                     1e-4) == "range_contract"
+
+
+def test_decoupled_workspace_is_chunked():
+    """The decoupled baseline keeps its N^2 intermediates (S_aug fp32, P_aug fp16) for one chunk
+    of heads at a time: the workspace grows with the chunk, not with batch x heads."""
+    from paper_2504_02211_b200 import _lib
+    small = _desc(mode=3, batch=1, heads=1, seq_len=8192, head_dim=128)
+    big = _desc(mode=3, batch=32, heads=32, seq_len=8192, head_dim=128)
+    ws1 = _lib.lib.efta_attn_workspace_bytes(C.byref(small))
+    ws2 = _lib.lib.efta_attn_workspace_bytes(C.byref(big))
+    per_head = (64 * 132) ** 2 * 4  # S_aug alone
+    assert ws1 > per_head
+    assert ws2 <= (4 << 30) + 256 and ws2 >= ws1
