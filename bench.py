@@ -274,6 +274,28 @@ def suite(dev):
                    "ft_overhead_pct": round((ms_p / ms_u - 1) * 100, 2), "ms": round(ms_p, 3)})
     out["c5_layer_sweep"] = c5
     out["c5_detections"] = lp.report().detections
+    del lp, lu, xx
+    torch.cuda.empty_cache()
+    # EFTA-optimized vs the decoupled baseline (csrc/decoupled.cu: traditional two-sided block
+    # ABFT around cuBLAS GEMMs, DMR softmax, N^2 intermediates in HBM) on the paper's Table 1 / 2
+    # head configurations at 16K tokens
+    dec = []
+    for (b, h, s_, d) in ((8, 16, 2048, 64), (1, 16, 16384, 64), (2, 32, 8192, 128)):
+        q = synth_inputs(31, (b, h, s_, d), dev)
+        k = synth_inputs(32, (b, h, s_, d), dev)
+        v = synth_inputs(33, (b, h, s_, d), dev)
+        row = {"batch": b, "heads": h, "seq_len": s_, "head_dim": d}
+        for mode, th in (("efta-opt", thr), ("decoupled", Thresholds(7e-6, 1e-3, 5e-3))):
+            op = EftaAttention(b, h, s_, d, mode=mode, thr=th, device=dev)
+            ms = _time_cuda(lambda: op(q, k, v), iters=3)
+            row[f"{mode}_ms"] = round(ms, 3)
+            row[f"{mode}_detections"] = op.report().detections
+            del op
+            torch.cuda.empty_cache()
+        row["efta_opt_speedup"] = round(row["decoupled_ms"] / row["efta-opt_ms"], 2)
+        dec.append(row)
+        del q, k, v
+    out["decoupled_vs_efta_opt"] = dec
     return out
 
 

@@ -56,7 +56,7 @@ struct Thresholds {
     static Thresholds observe();
 };
 
-enum class FTMode { NONE, EFTA, EFTA_OPTIMIZED };
+enum class FTMode { NONE, EFTA, EFTA_OPTIMIZED, DECOUPLED };
 enum class CheckKind { SCORE_CHECKSUM, EXP_CHECKSUM, FACTOR_RANGE, ROWSUM_RANGE, OUTPUT_CHECKSUM };
 enum class VerifyStatus { CLEAN, CORRECTED, DETECTED_UNCORRECTABLE, NONFINITE };
 enum class FaultSite { GEMM1_OUT, SUB_MAX, EXP_OUT, REDUCE_MAX, REDUCE_SUM, RESCALE_FACTOR,
@@ -187,6 +187,14 @@ std::pair<Matrix, FTReport> efta_forward(const Matrix& q, const Matrix& k, const
                                          const AttnConfig& cfg, const Thresholds& thr, FTMode mode,
                                          FaultInjector* inj = nullptr,
                                          const KernelKnobs* knobs = nullptr);
+
+// decoupled_ft_forward (include/efta/efta.hpp:94-96): the three-kernel baseline (traditional
+// two-sided block ABFT around the two GEMMs, DMR softmax, N^2 intermediates in HBM) on the GPU
+// (csrc/decoupled.cu); the same as efta_forward(..., FTMode::DECOUPLED, ...).
+std::pair<Matrix, FTReport> decoupled_ft_forward(const Matrix& q, const Matrix& k, const Matrix& v,
+                                                 const AttnConfig& cfg, const Thresholds& thr,
+                                                 FaultInjector* inj = nullptr,
+                                                 const KernelKnobs* knobs = nullptr);
 
 // ---- strided ABFT primitives (include/efta/abft.hpp:38-77), computed on the GPU ----
 // encode_strided: c1/c2 (rows x stride) of t, fp32 sums in the reference's order (bit-exact).

@@ -71,6 +71,7 @@ const char* ft_mode_name(FTMode m) {
         case FTMode::NONE: return "none";
         case FTMode::EFTA: return "efta";
         case FTMode::EFTA_OPTIMIZED: return "efta-opt";
+        case FTMode::DECOUPLED: return "decoupled";
     }
     return "?";
 }
@@ -78,6 +79,7 @@ std::optional<FTMode> ft_mode_from_name(const std::string& n) {
     if (n == "none") return FTMode::NONE;
     if (n == "efta") return FTMode::EFTA;
     if (n == "efta-opt" || n == "efta_optimized") return FTMode::EFTA_OPTIMIZED;
+    if (n == "decoupled") return FTMode::DECOUPLED;
     return std::nullopt;
 }
 const char* fault_site_name(FaultSite s) { return kSiteNames[static_cast<int>(s)]; }
@@ -237,7 +239,7 @@ std::pair<Matrix, FTReport> efta_forward(const Matrix& q, const Matrix& k, const
         for (const FaultSpec& f : inj->plan().specs)
             faults.push_back({0, static_cast<int>(f.site), f.block_i, f.block_j, f.row, f.col, f.bit,
                               f.trigger});
-    const int ev_cap = 4 * cfg.num_blocks() * (cfg.num_blocks() + 2) + 64;
+    const int ev_cap = 4 * cfg.num_blocks() * (cfg.num_blocks() + 2) + 64 + (mode == FTMode::DECOUPLED ? 4 * n : 0);
     std::vector<efta_event> events(ev_cap);
     std::vector<efta_fired> fired(64);
     efta_counters cnt{};
@@ -293,6 +295,12 @@ std::pair<Matrix, FTReport> efta_forward(const Matrix& q, const Matrix& k, const
         }
     }
     return {std::move(out), std::move(rep)};
+}
+
+std::pair<Matrix, FTReport> decoupled_ft_forward(const Matrix& q, const Matrix& k, const Matrix& v,
+                                                 const AttnConfig& cfg, const Thresholds& thr, FaultInjector* inj,
+                                                 const KernelKnobs* knobs) {
+    return efta_forward(q, k, v, cfg, thr, FTMode::DECOUPLED, inj, knobs);
 }
 
 // ------------------------------------------------------------------ strided ABFT on the GPU
