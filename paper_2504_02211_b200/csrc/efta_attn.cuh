@@ -71,15 +71,15 @@ struct AttnParams {
 // EFTA_TSQ stamps all four warps of a row warpgroup at slots 16 + base + warp quarter
 #define EFTA_TS(slot, j)                                                                       \
     do {                                                                                       \
-        if (p.prof && blockIdx.x == 2 && blockIdx.y == 5 &&                                    \
+        if (p.prof && blockIdx.x == 2 && blockIdx.y == (gridDim.y > 1 ? 5 : 0) &&             \
             (threadIdx.x & 31) == 0 && (j) >= 0 && (j) < 64)                                   \
-            p.prof[(j) * 32 + (slot)] = clock64();                                             \
+            p.prof[(j) * 64 + (slot)] = clock64();                                             \
     } while (0)
 #define EFTA_TSQ(base, j)                                                                      \
     do {                                                                                       \
-        if (p.prof && blockIdx.x == 2 && blockIdx.y == 5 &&                                    \
+        if (p.prof && blockIdx.x == 2 && blockIdx.y == (gridDim.y > 1 ? 5 : 0) &&             \
             (threadIdx.x & 31) == 0 && (j) >= 0 && (j) < 64)                                   \
-            p.prof[(j) * 32 + 16 + (base) + ((threadIdx.x >> 5) & 3)] = clock64();              \
+            p.prof[(j) * 64 + 16 + (base) + ((threadIdx.x >> 5) & 3)] = clock64();              \
     } while (0)
 #else
 #define EFTA_TS(slot, j) do { } while (0)

@@ -35,10 +35,13 @@
 // (warpgroup, warp quarter) an early and a late chain barrier (32 arrivals). Named
 // barriers: warpgroup 0 uses the single-warpgroup ids 1..7, warpgroup 1 the same +
 // kBarAltOfs (9, 10, 11, 14 in the loop; 9, 12, 13, 15 in the epilogue).
-// Tile boundary: the chain slots (early / late / lchain) and the fin slot hold one value
-// each. Warpgroup 0's block 0 of tile k+1 does not depend on warpgroup 1 otherwise, so it
-// waits on `ack` (per warp quarter, arrived by warpgroup 1 once it has read the last chain
-// values and fin of tile k, at its epilogue) before it publishes anything for tile k+1.
+// Tile boundary: the chain slots (early / late / lchain), the fin slot and their barriers are
+// double-buffered by tile parity, so warpgroup 0 starts tile k+1 while warpgroup 1 still runs
+// tile k's last block and epilogue (a single set made warpgroup 0 wait for that hand-over at
+// every tile boundary: ~20% of a 16-block tile). For n >= 4 warpgroup 0 cannot reach tile k+2
+// before warpgroup 1 has left tile k (its block 2 of tile k+1 waits on warpgroup 1's block 1);
+// for n == 2 nothing else bounds it, so block 0 of tile k waits on `ack` of tile k-2 (arrived
+// by warpgroup 1 once it has read tile k-2's chain values and fin, at its epilogue).
 //
 // INJ (fault-tap build, `debug` calls): the same schedule with the reference's explicit op
 // sequence (src/efta.cpp:125-257) so every FaultSite can be tapped by the thread owning the
@@ -101,7 +104,7 @@ __device__ __noinline__ float pair_linear_residual(const AttnParams& p, const fl
 }
 
 template <int D, bool PROT, bool INJ>
-__device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, uint64_t* s_full,
+__device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, float* ostage, uint64_t* s_full,
                                         uint64_t* s_free, uint64_t* p_ready, uint64_t* o_done, uint64_t* o_final,
                                         uint64_t* mx_early, uint64_t* mx_late, uint64_t* fin_bar, uint64_t* ack_bar,
                                         uint64_t* o_free, uint32_t tmem, int warp, int lane, int n,
@@ -123,10 +126,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         rs.dbl = reinterpret_cast<double*>(r + 128 * sizeof(RowSlot) + 16 * sizeof(int));
     }
     ThreadTap tap{};  // INJ: this row's fault spec of the current tile
-    uint64_t* my_early = mx_early + w * 4 + wq;
-    uint64_t* my_late = mx_late + w * 4 + wq;
-    uint64_t* pa_early = mx_early + (1 - w) * 4 + wq;
-    uint64_t* pa_late = mx_late + (1 - w) * 4 + wq;
+    AltXch* const xcb = xc;  // [tile parity]
     const float scale = p.scale, scale_log2 = p.scale_log2;
     const uint32_t s_addr = lane_base + L::COL_S0 + w * L::SW;
     const uint32_t cs_addr = s_addr + 128;  // c1_hi (8) | c1_lo (8)
@@ -161,6 +161,15 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     const int u = pair_next_tile(tinfo, t_full, t_empty, k, true);
     if (u < 0) break;
     const int head = u / npq, qt = 2 * (u % npq) + static_cast<int>(rank);
+    // this tile's chain slots and barriers (tile parity); each barrier completes one phase per
+    // block of its warpgroup in the tiles of this parity
+    const int par = k & 1;
+    xc = xcb + par;
+    uint64_t* my_early = mx_early + par * 8 + w * 4 + wq;
+    uint64_t* my_late = mx_late + par * 8 + w * 4 + wq;
+    uint64_t* pa_early = mx_early + par * 8 + (1 - w) * 4 + wq;
+    uint64_t* pa_late = mx_late + par * 8 + (1 - w) * 4 + wq;
+    const int ph0 = (k >> 1) * npq;  // blocks per warpgroup in the earlier tiles of this parity
     const int seq_row0 = head * p.seq_len;
     if constexpr (INJ) tap.load(p, head, qt, row);
     // own sums, referenced to m_ref (the reference max of this warpgroup's last block);
@@ -168,12 +177,12 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     float l_w = 0.0f, lb_w = 0.0f, m_ref = -CUDART_INF_F, m_true_last = -CUDART_INF_F;
     for (int j = w; j < n; j += 2, ++it) {
         const int g = k * n + j;
-        if ((warp & 3) == 0) EFTA_TS(0, j);
+        if ((warp & 3) == 0) EFTA_TS(0, g);
         mbar_wait(&s_full[w], it & 1);
-        if ((warp & 3) == 0) EFTA_TS(1, j);
-        EFTA_TSQ(8, j);
+        if ((warp & 3) == 0) EFTA_TS(1, g);
+        EFTA_TSQ(8, g);
         tc_fence_after();
-        const uint32_t pph = static_cast<uint32_t>((g - 1) >> 1) & 1u;  // partner's phase for block g-1
+        const uint32_t pph = static_cast<uint32_t>(ph0 + ((j - 1) >> 1)) & 1u;  // partner's phase for block j-1
         const int tap_snap = tap.count;
         float pv[kBlock];
         float m_true_prev = -CUDART_INF_F, m_run_prev = -CUDART_INF_F;
@@ -253,13 +262,14 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                 m_new = (j == 0 || m_true - m_run_prev > kLazyTau) ? m_true : m_run_prev;
             }
             if (attempt == 0) {
-                // tile boundary: warpgroup 1 has consumed the previous tile's chain / fin slots
-                if (w == 0 && j == 0 && k > 0) mbar_wait(&ack_bar[wq], static_cast<uint32_t>(k - 1) & 1u);
+                // tile boundary (n == 2 only binds): warpgroup 1 has consumed tile k-2's slots
+                if (w == 0 && j == 0 && k >= 2)
+                    mbar_wait(&ack_bar[par * 4 + wq], static_cast<uint32_t>((k >> 1) - 1) & 1u);
                 xc->early[w][row] = make_float2(m_true, m_new);
                 mbar_arrive(my_early);
             }
-            if ((warp & 3) == 0) EFTA_TS(15, j);
-            EFTA_TSQ(4, j);
+            if ((warp & 3) == 0) EFTA_TS(15, g);
+            EFTA_TSQ(4, g);
             float pc1v[kStride];
             float2 prod_f[kStride / 2];
             if (PROT) {
@@ -340,14 +350,14 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             // ---- late chain check: did the partner's decision revise block j-1's maxima?
             bool chain_bad = false;
             if (j > 0) {
-                if ((warp & 3) == 0) EFTA_TS(8, j);
+                if ((warp & 3) == 0) EFTA_TS(8, g);
                 if (attempt == 0) mbar_wait(pa_late, pph);
                 const float2 c = lds_f2(&xc->late[1 - w][row]);
                 chain_bad = __float_as_uint(c.x) != __float_as_uint(m_true_prev) ||
                             __float_as_uint(c.y) != __float_as_uint(m_run_prev);
             }
-            if ((warp & 3) == 0) EFTA_TS(9, j);
-            EFTA_TSQ(0, j);
+            if ((warp & 3) == 0) EFTA_TS(9, g);
+            EFTA_TSQ(0, g);
             if (!named_bar_or(6 + bo, 128, exp_affected || factor_bad || chain_bad)) break;
             if (named_bar_or(6 + bo, 128, chain_bad)) continue;  // redo the block with the revised maxima
             // ---- rare: the reference recovery ladder for this tile
@@ -407,14 +417,14 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&s_free[w], 0);
-        if ((warp & 3) == 0) EFTA_TS(2, j);
+        if ((warp & 3) == 0) EFTA_TS(2, g);
         // ---- factors: fo for the shared O accumulator (chain), fw for this warpgroup's sums
         const float fo = ex2_approx((m_run_prev - m_new) * kLog2e);
         const float fw = ex2_approx((m_ref - m_new) * kLog2e);
         if (PROT) lb_w = __fadd_rn(__fmul_rn(lb_w, fw), ex2_approx((bm - m_new) * kLog2e));
         if constexpr (!INJ) l_w = __fadd_rn(__fmul_rn(fw, l_w), row_psum());
 
-        if ((warp & 3) == 0) EFTA_TS(3, j);
+        if ((warp & 3) == 0) EFTA_TS(3, g);
         // ---- P (fp16): packed first, stored once the P buffer is free (P.V of block j-1
         // with one shared buffer, of block j-2 with one buffer per warpgroup)
         uint32_t pk[64];
@@ -432,12 +442,12 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             need_o = need_o || __any_sync(0xffffffffu, t_acc || t_res || t_res0);
         }
         if (L::NPB == 1 ? (g > 0) : (g >= 2 || need_o)) {
-            if ((warp & 3) == 0) EFTA_TS(4, j);
+            if ((warp & 3) == 0) EFTA_TS(4, g);
             if (L::NPB == 1 || need_o)
                 mbar_wait(&o_done[1 - w], static_cast<uint32_t>((g - 1) >> 1) & 1u);
             else
                 mbar_wait(&o_done[w], static_cast<uint32_t>((g - 2) >> 1) & 1u);
-            if ((warp & 3) == 0) EFTA_TS(5, j);
+            if ((warp & 3) == 0) EFTA_TS(5, g);
             tc_fence_after();
         }
         if constexpr (kWideTmem) {
@@ -475,8 +485,8 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         tmem_wait_st();
         tc_fence_before();
         signal_p_ready<true>(&p_ready[w], lane);
-        if ((warp & 3) == 0) EFTA_TS(6, j);
-        EFTA_TSQ(12, j);
+        if ((warp & 3) == 0) EFTA_TS(6, g);
+        EFTA_TSQ(12, g);
         m_ref = m_new;
         m_true_last = m_true;
     }
@@ -486,13 +496,16 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     // epilogue while warpgroup 0 already starts the next tile.
     if (w == 0) {
         xc->fin[row] = make_float4(INJ ? 0.0f : l_w, lb_w, m_ref, m_true_last);
-        mbar_arrive(&fin_bar[wq]);
+        mbar_arrive(&fin_bar[par * 4 + wq]);
         if (INJ) flush_families(0.0f);
         continue;
     }
-    mbar_wait(&fin_bar[wq], static_cast<uint32_t>(k) & 1u);
+    const int g_last = k * n + n - 1;
+    if ((warp & 3) == 0) EFTA_TS(32, g_last);
+    mbar_wait(&fin_bar[par * 4 + wq], static_cast<uint32_t>(k >> 1) & 1u);
+    if ((warp & 3) == 0) EFTA_TS(33, g_last);
     const float4 fb = lds_f4(&xc->fin[row]);
-    mbar_arrive(&ack_bar[wq]);  // this tile's chain and fin slots are consumed
+    mbar_arrive(&ack_bar[par * 4 + wq]);  // this tile's chain and fin slots are consumed
     float m_run = m_ref;  // the chain's final reference max (block n-1 is ours)
     const float m_true = m_true_last;
     const float fbf = ex2_approx((fb.z - m_run) * kLog2e);
@@ -501,6 +514,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
 
     // ------------------------------------------------ epilogue (as row_wg, warpgroup 1)
     mbar_wait(o_final, static_cast<uint32_t>(k) & 1u);
+    if ((warp & 3) == 0) EFTA_TS(34, g_last);
     tc_fence_after();
     float o[D];
     float c1[kStride], c2[kStride];
@@ -522,6 +536,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive_cluster(o_free, 0);
+    if ((warp & 3) == 0) EFTA_TS(35, g_last);
     if constexpr (INJ) tap_row<D>(tap, p, EFTA_GEMM2_ACC, n - 1, o);
     {
         // bring O, its checksums, l and the lower bound from the lazy reference max to
@@ -573,6 +588,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             wg_sync(bo);
         }
     }
+    if ((warp & 3) == 0) EFTA_TS(36, g_last);
     // normalization (efta.cpp:312-327): one IEEE reciprocal, then products (within 1 ulp of
     // the reference's division); the tap build keeps the reference's division [NORMALIZE_OUT]
     if constexpr (INJ) {
@@ -595,18 +611,43 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         }
     }
     float fam_out = 0.0f;
+    if ((warp & 3) == 0) EFTA_TS(40, g_last);
     if (PROT) {
         float res;
         verify_output_tile<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res, bo);
         if (isfinite(res)) fam_out = res;
     }
+    if ((warp & 3) == 0) EFTA_TS(37, g_last);
     const size_t grow = static_cast<size_t>(seq_row0) + qt * kBlock + row;
-    float4* dst = reinterpret_cast<float4*>(p.o + grow * D);
+    {
+        // coalesced O store: thread = row holds D fp32; the warp stages 32 rows x 16 columns at
+        // a time through shared memory (16-byte chunks XOR-swizzled by row: conflict-free both
+        // ways) and writes them back as full 64-byte row segments, 8 rows per instruction
+        // (a row per thread made every 16-byte store touch 32 lines: an LSU-bound epilogue)
+        float* stg = ostage + wq * 512;
+        float* obase = p.o + (grow - lane) * D;  // row 0 of this warp
 #pragma unroll
-    for (int c = 0; c < D / 4; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+        for (int c = 0; c < D / 16; ++c) {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4)
+                *reinterpret_cast<float4*>(stg + lane * 16 + ((q4 ^ (lane & 3)) << 2)) =
+                    make_float4(o[c * 16 + 4 * q4], o[c * 16 + 4 * q4 + 1], o[c * 16 + 4 * q4 + 2],
+                                o[c * 16 + 4 * q4 + 3]);
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = 8 * i + (lane >> 2), q4 = lane & 3;
+                const float4 v = *reinterpret_cast<const float4*>(stg + r * 16 + ((q4 ^ (r & 3)) << 2));
+                *reinterpret_cast<float4*>(obase + static_cast<size_t>(r) * D + c * 16 + 4 * q4) = v;
+            }
+            __syncwarp();
+        }
+    }
     if (p.m_out) p.m_out[grow] = m_run;
     if (p.l_out) p.l_out[grow] = l_run;
+    if ((warp & 3) == 0) EFTA_TS(38, g_last);
     flush_families(fam_out);
+    if ((warp & 3) == 0) EFTA_TS(39, g_last);
     }  // tiles
     (void)MODE;
 }

@@ -48,15 +48,16 @@ struct PairLayout {
     static constexpr uint32_t OFF_V = OFF_K + KS * K_STAGE;
     static constexpr uint32_t OFF_BAR = OFF_V + VS * V_STAGE;
     // q_full, k_full/empty[KS], v_full/empty[VS], s_full[2], s_free[2], p_ready[2],
-    // o_done[2], o_final, chain barriers mx_early[2][4], mx_late[2][4], q_empty[2], o_free, fin[4],
-    // second q_full, tile ring full[4] / empty[4], tile-boundary ack[4]
-    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2 + 2 + 2 + 1 + 16 + 2 + 1 + 4 + 1 + 8 + 4;
+    // o_done[2], o_final, chain barriers mx_early[2 tile parity][2][4], mx_late[2][2][4], q_empty[2],
+    // o_free, fin[2][4], second q_full, tile ring full[4] / empty[4], tile-boundary ack[2][4]
+    static constexpr int NBAR = 1 + 2 * KS + 2 * VS + 2 + 2 + 2 + 2 + 1 + 32 + 2 + 1 + 8 + 1 + 8 + 8;
     static constexpr uint32_t OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
     static constexpr uint32_t RED_BYTES = 128 * 24 + 256;  // per row warpgroup
     static constexpr uint32_t OFF_XCH = OFF_RED + 2 * RED_BYTES;
-    static constexpr uint32_t OFF_TINFO = OFF_XCH + 7168;  // tile ring: int[4]
-    static constexpr uint32_t SMEM_BYTES = OFF_TINFO + 16 + 1024;
+    static constexpr uint32_t OFF_TINFO = OFF_XCH + 2 * 7168;  // chain exchange x tile parity; tile ring: int[4]
+    static constexpr uint32_t OFF_OSTG = OFF_TINFO + 16;       // epilogue O staging: 4 warps x 32 x 16 fp32
+    static constexpr uint32_t SMEM_BYTES = OFF_OSTG + 4 * 2048 + 1024;
     // TMEM columns
     static constexpr uint32_t COL_S0 = 0, COL_O = 2 * SW, COL_P = COL_O + VROWS, TMEM_COLS = 512;
     // one P buffer per row warpgroup when it fits (unprotected d=128, every d=64 variant);
@@ -203,15 +204,15 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     uint64_t* p_ready = s_free + 2;    // [2] P_j stored / O rescaled (leader)
     uint64_t* o_done = p_ready + 2;    // [2] P.V of block j complete
     uint64_t* o_final = o_done + 2;
-    uint64_t* mx_early = o_final + 1;  // [2][4]
-    uint64_t* mx_late = mx_early + 8;  // [2][4]
-    uint64_t* q_empty = mx_late + 8;   // [2] every score MMA of the tile using Q buffer b done
+    uint64_t* mx_early = o_final + 1;  // [tile parity][warpgroup][warp quarter]
+    uint64_t* mx_late = mx_early + 16; // [2][2][4]
+    uint64_t* q_empty = mx_late + 16;  // [2] every score MMA of the tile using Q buffer b done
     uint64_t* o_free = q_empty + 2;    // the epilogue read O (leader; 4 warps x 2 CTAs)
-    uint64_t* fin_bar = o_free + 1;    // [4] warpgroup 0's sums of the tile (per warp quarter)
-    uint64_t* q_full2 = fin_bar + 4;   // q_full of Q buffer 1 (q_full is buffer 0's)
+    uint64_t* fin_bar = o_free + 1;    // [tile parity][4] warpgroup 0's sums of the tile (per warp quarter)
+    uint64_t* q_full2 = fin_bar + 8;   // q_full of Q buffer 1 (q_full is buffer 0's)
     uint64_t* t_full = q_full2 + 1;    // [4] tile ring slot published (this CTA)
     uint64_t* t_empty = t_full + 4;    // [4] tile ring slot consumed by all 21 warps (leader)
-    uint64_t* ack_bar = t_empty + 4;   // [4] warpgroup 1 consumed the tile's chain / fin slots (per warp quarter)
+    uint64_t* ack_bar = t_empty + 4;   // [tile parity][4] warpgroup 1 consumed the tile's chain / fin slots
     int* tinfo = reinterpret_cast<int*>(smem + L::OFF_TINFO);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
@@ -233,13 +234,13 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             mbar_init(&o_done[b], 1);
         }
         mbar_init(o_final, 1);
-        for (int i = 0; i < 16; ++i) mbar_init(&mx_early[i], 32);
+        for (int i = 0; i < 32; ++i) mbar_init(&mx_early[i], 32);  // early and late, both parities
         mbar_init(&q_empty[0], 1);
         mbar_init(&q_empty[1], 1);
         mbar_init(q_full2, 1);
         for (int i = 0; i < kTileRing; ++i) { mbar_init(&t_full[i], 1); mbar_init(&t_empty[i], kTileConsumers); }
         mbar_init(o_free, 8);
-        for (int i = 0; i < 4; ++i) { mbar_init(&fin_bar[i], 32); mbar_init(&ack_bar[i], 32); }
+        for (int i = 0; i < 8; ++i) { mbar_init(&fin_bar[i], 32); mbar_init(&ack_bar[i], 32); }
         fence_barrier_init();
         tma_prefetch_desc(&tm_q);
         tma_prefetch_desc(&tm_ka);
@@ -367,7 +368,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                 for (int j = 0; j < n; ++j, ++g) {
                     if (g >= 2) {
                         mbar_wait(&s_free[g & 1], ((g - 2) >> 1) & 1);
-                        EFTA_TS(7, j - 2);
+                        EFTA_TS(7, g - 2);
                     }
                     const int s = g % KS;
                     mbar_wait(&k_full[s], (g / KS) & 1);
@@ -386,7 +387,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                         if (j == n - 1) commit2_both(&q_empty[qb]);
                     }
                     __syncwarp();
-                    EFTA_TS(11, j - 2);
+                    EFTA_TS(11, g - 2);
                 }
             }
         }
@@ -401,13 +402,13 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             for (int k = 0;; ++k) {
                 if (pair_next_tile(tinfo, t_full, t_empty, k, true) < 0) break;
                 for (int j = 0; j < n; ++j, ++g) {
-                    EFTA_TS(10, j);
+                    EFTA_TS(10, g);
                     mbar_wait(&p_ready[g & 1], (g >> 1) & 1);
-                    EFTA_TS(12, j);
+                    EFTA_TS(12, g);
                     tc_fence_after();
                     const int s = g % VS;
                     mbar_wait(&v_full[s], (g / VS) & 1);
-                    EFTA_TS(14, j);
+                    EFTA_TS(14, g);
                     if (j == 0 && k > 0) mbar_wait(o_free, (k - 1) & 1);  // the last epilogue read O
                     tc_fence_after();
                     const uint64_t dv = dv0 + ((s * L::V_STAGE) >> 4);
@@ -423,14 +424,15 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                         if (j == n - 1) commit2_both(o_final);
                     }
                     __syncwarp();
-                    EFTA_TS(13, j);
+                    EFTA_TS(13, g);
                 }
             }
         }
         __syncwarp();
     } else {
         setmaxnreg_inc<232>();
-        row_alt<D, PROT, INJ>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH), s_full,
+        row_alt<D, PROT, INJ>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH),
+                              reinterpret_cast<float*>(smem + L::OFF_OSTG), s_full,
                               s_free, p_ready, o_done, o_final, mx_early, mx_late, fin_bar, ack_bar, o_free, tmem,
                               warp, lane, n, tinfo, t_full, t_empty, rank);
     }

@@ -294,7 +294,7 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
 #ifdef EFTA_PROF
     {
         static unsigned long long* prof_buf = nullptr;
-        if (!prof_buf) cudaMalloc(&prof_buf, 64 * 32 * sizeof(unsigned long long));
+        if (!prof_buf) cudaMalloc(&prof_buf, 64 * 64 * sizeof(unsigned long long));
         p.prof = prof_buf;
         efta_prof_buffer_ptr = prof_buf;
     }
