@@ -16,7 +16,9 @@
 //   [W rows 128..255| Wc_lo rows 0..15] -> TMEM cols [144, 288)
 // so A is read twice per k-step and the checksum work is 32/256 = 12.5% extra MMA.
 // Persistent grid (one CTA per SM), static round-robin tile order (m-major rows of
-// n-tiles so consecutive CTAs share X rows in L2). The single 288-column accumulator is
+// n-tiles so consecutive CTAs share X rows in L2). Output rows leave through a per-warp
+// shared-memory staging buffer as full 128-byte row segments (a row per thread made every
+// 16-byte store touch 32 lines: the stores were LSU-bound and delayed the next tile's drain). The single 288-column accumulator is
 // drained by 8 epilogue warps: warps 4-7 own output columns 0..127 of their rows, warps
 // 8-11 columns 128..255 (same TMEM lanes); the upper half hands its partial strided sums
 // (groups l = 16..31) to the lower half through shared memory, which verifies the row.
@@ -36,7 +38,10 @@ using namespace efta_sm100;
 namespace {
 
 constexpr int GM = 128, GN = 256, GK = 64;   // tile and k-chunk
-constexpr int STAGES = 4;
+#ifndef ABFT_STAGES
+#define ABFT_STAGES 3
+#endif
+constexpr int STAGES = ABFT_STAGES;  // 3 x 52 KB (+ the epilogue staging buffers); 4 stages left no room for them
 constexpr uint32_t A_BYTES = GM * GK * 2;            // 16 KB
 constexpr uint32_t B_HALF = (128 + 16) * GK * 2;     // 18 KB: 128 W rows + 16 checksum rows
 constexpr uint32_t B_BYTES = 2 * B_HALF;             // 36 KB
@@ -45,7 +50,9 @@ constexpr uint32_t OFF_BAR = STAGES * STAGE;
 constexpr uint32_t OFF_TMEM = OFF_BAR + (2 * STAGES + 2) * 8;
 constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
 constexpr uint32_t OFF_XS = OFF_RED + 128 * 24 + 256;  // column half 1's partial strided sums [128][16]
-constexpr uint32_t SMEM_BYTES = OFF_XS + 128 * 16 * 4 + 16 + 1024;
+constexpr uint32_t OFF_STG = (OFF_XS + 128 * 16 * 4 + 16 + 127) & ~127u;  // epilogue staging: 8 warps x 4 KB
+constexpr uint32_t SMEM_BYTES = OFF_STG + 8 * 4096 + 1024;
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 constexpr int GEMM_THREADS = 384;  // warps 0-3: TMA / MMA / idle / idle; 4-11: epilogue (2 column halves)
 
 struct GemmParams {
@@ -202,23 +209,40 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                     nonfin |= !isfinite(val);
                 }
             }
-            // fp16 output of this half: packed and stored once the accumulator is released
+            // this half's output row segment (fp16 or fp32), stored once the accumulator is
+            // released: the warp stages 32 rows x 128 bytes at a time (16-byte chunks
+            // XOR-swizzled by row) and writes 4 full row segments per instruction
             auto store_half = [&]() {
-                if constexpr (F32) {
-                    float4* dst = reinterpret_cast<float4*>(yrow32 + half * 128);
+                uint32_t* stg = reinterpret_cast<uint32_t*>(smem + OFF_STG) + (warp - 4) * 1024;
+                constexpr int NCH = F32 ? 4 : 2;  // 128-byte chunks per half row
+                uint8_t* rowbase = F32 ? reinterpret_cast<uint8_t*>(yrow32 + half * 128)
+                                       : reinterpret_cast<uint8_t*>(yrow + half * 128);
+                const size_t row_pitch = static_cast<size_t>(p.n) * (F32 ? 4 : 2);
+                uint8_t* warp_base = rowbase - static_cast<size_t>(lane) * row_pitch;  // row 0 of the warp
 #pragma unroll
-                    for (int x = 0; x < 32; ++x) dst[x] = make_float4(v[4 * x], v[4 * x + 1], v[4 * x + 2], v[4 * x + 3]);
-                    return;
-                }
+                for (int c = 0; c < NCH; ++c) {
 #pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) {
-                    uint4 pk[4];
-                    uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+                    for (int q4 = 0; q4 < 8; ++q4) {
+                        uint4 w4;
+                        if constexpr (F32) {
+                            w4 = make_uint4(__float_as_uint(v[c * 32 + 4 * q4]), __float_as_uint(v[c * 32 + 4 * q4 + 1]),
+                                            __float_as_uint(v[c * 32 + 4 * q4 + 2]),
+                                            __float_as_uint(v[c * 32 + 4 * q4 + 3]));
+                        } else {
+                            const int b = c * 64 + 8 * q4;
+                            w4 = make_uint4(pack_half2(v[b], v[b + 1]), pack_half2(v[b + 2], v[b + 3]),
+                                            pack_half2(v[b + 4], v[b + 5]), pack_half2(v[b + 6], v[b + 7]));
+                        }
+                        *reinterpret_cast<uint4*>(stg + lane * 32 + ((q4 ^ (lane & 7)) << 2)) = w4;
+                    }
+                    __syncwarp();
 #pragma unroll
-                    for (int x = 0; x < 16; ++x) pw[x] = pack_half2(v[c4 * 32 + 2 * x], v[c4 * 32 + 2 * x + 1]);
-                    uint4* dst = reinterpret_cast<uint4*>(yrow + (half * 4 + c4) * 32);
-#pragma unroll
-                    for (int x = 0; x < 4; ++x) dst[x] = pk[x];
+                    for (int i = 0; i < 8; ++i) {
+                        const int r = 4 * i + (lane >> 3), q4 = lane & 7;
+                        const uint4 w4 = *reinterpret_cast<const uint4*>(stg + r * 32 + ((q4 ^ (r & 7)) << 2));
+                        *reinterpret_cast<uint4*>(warp_base + static_cast<size_t>(r) * row_pitch + c * 128 + q4 * 16) = w4;
+                    }
+                    __syncwarp();
                 }
             };
             if (half == 1) {

@@ -185,6 +185,10 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         const uint32_t pph = static_cast<uint32_t>(ph0 + ((j - 1) >> 1)) & 1u;  // partner's phase for block j-1
         const int tap_snap = tap.count;
         float pv[kBlock];
+        // P packed to fp16x2 for the P.V MMA. The fast build packs inside the exp loop, so the
+        // fp32 row dies there (pv = S, pk = P: 192 live registers otherwise); its rare path
+        // rebuilds the fp32 P from the still-resident S (exp_rebuild)
+        uint32_t pk[64];
         float m_true_prev = -CUDART_INF_F, m_run_prev = -CUDART_INF_F;
         float m_true, m_new, bm, psum_f = 0.0f;
         bool replaced_p = false;
@@ -308,8 +312,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                         e.x = ex2_approx(a.x);
                         e.y = ex2_approx(a.y);
                     }
-                    pv[c] = e.x;
-                    pv[c + 1] = e.y;
+                    pk[c >> 1] = pack_half2(e.x, e.y);
                     if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
                     else ps0 = fadd2(ps0, e);
                     if (PROT) {
@@ -372,15 +375,42 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                 if (degenerate) { exp_res = CUDART_INF_F; exp_viol = 1; }
             }
             float p_loc[kBlock];
+            if constexpr (INJ) {
 #pragma unroll
-            for (int c = 0; c < kBlock; ++c) p_loc[c] = pv[c];
+                for (int c = 0; c < kBlock; ++c) p_loc[c] = pv[c];
+            } else {
+                // the fast path's fp32 P, rebuilt bit for bit from S (same fma, same exp split)
+                const float mL = m_new * kLog2e;
+                uint32_t r[32];
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    tmem_ld32(s_addr + c4 * 32, r);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int x = 0; x < 32; ++x)
+                        p_loc[c4 * 32 + x] = ex2_col<D>(c4 * 32 + x, fmaf(__uint_as_float(r[x]), scale_log2, -mL));
+                }
+            }
             int replaced = 0;
             exp_stage_slow<INJ, D, true>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res, exp_viol,
                                          m_run_prev, m_new, bm, p_loc, replaced, tap, sc_fault_col, sc_fault_val,
                                          rs, bo);
             if (replaced) {
+                if constexpr (INJ) {
 #pragma unroll
-                for (int c = 0; c < kBlock; ++c) pv[c] = p_loc[c];
+                    for (int c = 0; c < kBlock; ++c) pv[c] = p_loc[c];
+                } else {
+                    // repack, and re-sum with the fast path's pairing
+#pragma unroll
+                    for (int x = 0; x < 64; ++x) pk[x] = pack_half2(p_loc[2 * x], p_loc[2 * x + 1]);
+                    float2 ps0 = make_float2(p_loc[0], p_loc[1]), ps1 = make_float2(p_loc[2], p_loc[3]);
+#pragma unroll
+                    for (int c = 4; c < kBlock; c += 4) {
+                        ps0 = fadd2(ps0, make_float2(p_loc[c], p_loc[c + 1]));
+                        ps1 = fadd2(ps1, make_float2(p_loc[c + 2], p_loc[c + 3]));
+                    }
+                    psum_f = (ps0.x + ps0.y) + (ps1.x + ps1.y);
+                }
             }
             replaced_p = replaced != 0;
             m_true = (m_true_prev < m_new) ? m_new : m_true_prev;
@@ -389,7 +419,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         }
         // the partial row sum of P (re-summed with the fast path's pairing after a recompute)
         auto row_psum = [&]() {
-            if (!replaced_p) return psum_f;
+            if (!INJ || !replaced_p) return psum_f;  // the fast build re-summed in its rare path
             float2 ps0 = make_float2(pv[0], pv[1]), ps1 = make_float2(pv[2], pv[3]);
 #pragma unroll
             for (int c = 4; c < kBlock; c += 4) {
@@ -427,9 +457,10 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         if ((warp & 3) == 0) EFTA_TS(3, g);
         // ---- P (fp16): packed first, stored once the P buffer is free (P.V of block j-1
         // with one shared buffer, of block j-2 with one buffer per warpgroup)
-        uint32_t pk[64];
+        if constexpr (INJ) {
 #pragma unroll
-        for (int x = 0; x < 64; ++x) pk[x] = pack_half2(pv[2 * x], pv[2 * x + 1]);
+            for (int x = 0; x < 64; ++x) pk[x] = pack_half2(pv[2 * x], pv[2 * x + 1]);
+        }
         bool need_o = j > 0 && !__all_sync(0xffffffffu, fo == 1.0f);
         // INJ: the O accumulator taps of this block force the rescale pass: GEMM2_ACC of block
         // j-1 (after its P.V), RESCALE_FACTOR of block j, and of block 0 (deferred to block 1:
