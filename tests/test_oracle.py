@@ -260,3 +260,26 @@ def test_oracle_bit_exact_vs_reference_random_campaign():
                                             e["row"], e["col"]) for e in b.events]
             assert (a.detections, a.corrections, a.recomputes, a.failed) == \
                    (b.detections, b.corrections, b.recomputes, b.failed)
+
+
+# ---------------------------------------------------------------- decoupled baseline (reference)
+@pytest.mark.skipif(not os.path.exists(REF_SO), reason="oracle/_ref not built")
+def test_reference_decoupled_through_shim():
+    """The GPU decoupled baseline's checker (oracle/_ref, mode 3 -> decoupled_ft_forward): the
+    reference's own decoupled tests restated through the shim (tests/test_efta.cpp:248-313,
+    same geometry N=64 d=32 B=16, same thresholds): clean output equals two-pass attention
+    within 1e-3, and one upset per kernel is detected and repaired."""
+    from oracle import Oracle
+    ref = Oracle("ref")
+    for seed in (31, 32, 33):
+        q, k, v, _ = ref.gen_trial(seed, 64, 32, 16, 8)
+        r = ref.efta_forward(q, k, v, 16, 8, mode="decoupled", thr=(7e-6, 0.48, 0.48))
+        o = ref.standard_attention(q, k, v, 16, 8)
+        assert np.abs(r.o - o).max() < 1e-3 and r.detections == 0 and not r.failed
+    q, k, v, _ = ref.gen_trial(777, 64, 32, 16, 8)
+    thr = (7e-6, 1e-3, 5e-3)
+    clean = ref.efta_forward(q, k, v, 16, 8, mode="decoupled", thr=thr)
+    for spec in ("GEMM1_OUT:0:1:2:3:30", "EXP_OUT:1:1:3:4:30", "REDUCE_SUM:2:0:5:0:30", "GEMM2_ACC:1:0:2:7:30"):
+        r = ref.efta_forward(q, k, v, 16, 8, mode="decoupled", thr=thr, specs=[spec])
+        assert r.detections > 0 and not r.failed, spec
+        assert np.abs(r.o - clean.o).max() < 1e-3, spec
