@@ -40,7 +40,7 @@ extern "C" {
 #endif
 
 /* Attention problem: Q, K, V are [batch*heads, seq_len, head_dim] fp16 (bits as
- * uint16), O is fp32 of the same shape, m_out / l_out are [batch*heads, seq_len]
+ * uint16; K and V [batch*kv_heads, ...] with grouped-query attention), O is fp32 of Q's shape, m_out / l_out are [batch*heads, seq_len]
  * fp32 (the reference's FTReport::final_m / final_l). */
 typedef struct {
     int batch, heads, seq_len, head_dim;
@@ -57,6 +57,11 @@ typedef struct {
                            prepass; e.g. K/V reused across calls). On the CTA-pair path the
                            workspace also holds the transposed V operand ([V^T ; VC^T]), so the
                            flag covers V itself, in every mode. Ignored by the host path. */
+    int kv_heads;       /* grouped-query attention: K and V are [batch*kv_heads, seq_len, head_dim];
+                           query head h of a batch entry reads K/V head h / (heads / kv_heads).
+                           0 (or heads) = multi-head attention. Not a reference feature (SPEC.md:141,
+                           356 list GQA as a non-goal): each query head still runs the reference
+                           algorithm on its group's K and V. */
 } efta_attn_desc;
 
 const char* efta_last_error(void);

@@ -25,7 +25,8 @@ class AttnDesc(C.Structure):
                 ("head_dim", C.c_int), ("block", C.c_int), ("stride", C.c_int),
                 ("scale", C.c_float), ("mode", C.c_int), ("eps1", C.c_double),
                 ("eps2", C.c_double), ("eps_lin", C.c_double), ("observe_linear", C.c_int),
-                ("rowmax_bias", C.c_float), ("debug", C.c_int), ("checksums_ready", C.c_int)]
+                ("rowmax_bias", C.c_float), ("debug", C.c_int), ("checksums_ready", C.c_int),
+                ("kv_heads", C.c_int)]
 
 
 class FaultSpec(C.Structure):

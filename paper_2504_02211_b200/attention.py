@@ -122,10 +122,10 @@ class FTReport:
         return max(v) if v else -INF
 
 
-def _desc(b, h, s, d, mode, thr, scale, observe_linear, rowmax_bias, debug, block, stride):
+def _desc(b, h, s, d, mode, thr, scale, observe_linear, rowmax_bias, debug, block, stride, kv_heads=0):
     return _lib.AttnDesc(b, h, s, d, block, stride, float(scale), MODES[mode], float(thr.eps1),
                          float(thr.eps2), float(thr.eps_lin), 1 if observe_linear else 0,
-                         float(rowmax_bias), 1 if debug else 0, 0)
+                         float(rowmax_bias), 1 if debug else 0, 0, int(kv_heads))
 
 
 def _as_bhsd(x: torch.Tensor):
@@ -143,12 +143,14 @@ class EftaAttention:
 
     def __init__(self, batch, heads, seq_len, head_dim, mode="efta-opt", thr=None, scale=0.0,
                  observe_linear=False, rowmax_bias=0.0, debug=False, block=128, stride=8,
-                 ev_cap=4096, fired_cap=256, device="cuda"):
+                 ev_cap=4096, fired_cap=256, device="cuda", kv_heads=None):
         self.shape = (batch, heads, seq_len, head_dim)
+        # grouped-query attention: K / V carry kv_heads heads (query head h reads h // group)
+        self.kv_heads = heads if not kv_heads else int(kv_heads)
         self.mode = mode
         self.thr = thr or Thresholds()
         self.desc = _desc(batch, heads, seq_len, head_dim, mode, self.thr, scale, observe_linear,
-                          rowmax_bias, debug, block, stride)
+                          rowmax_bias, debug, block, stride, self.kv_heads)
         check(lib.efta_attn_validate(C.byref(self.desc)))
         ws = lib.efta_attn_workspace_bytes(C.byref(self.desc))
         dev = torch.device(device)
@@ -174,10 +176,10 @@ class EftaAttention:
 
     def __call__(self, q, k, v, o=None, m=None, l=None, stream=None):
         b, h, s, d = self.shape
-        for t in (q, k, v):
+        for t, hh in ((q, h), (k, self.kv_heads), (v, self.kv_heads)):
             if t.dtype != torch.float16 or not t.is_cuda or not t.is_contiguous():
                 raise _lib.ConfigError("efta_forward: q/k/v must be contiguous CUDA fp16 tensors")
-            if t.numel() != b * h * s * d:
+            if t.numel() != b * hh * s * d:
                 raise _lib.ConfigError("attention: Q/K/V must all be seq_len x head_dim")
         if o is None:
             o = torch.empty((b, h, s, d), dtype=torch.float32, device=q.device)
@@ -232,6 +234,7 @@ def efta_forward(q, k, v, mode="efta-opt", thr: Thresholds | None = None, faults
     shape = q.shape
     q4, k4, v4 = (_as_bhsd(x).contiguous() for x in (q, k, v))
     b, h, s, d = q4.shape
+    kv_heads = k4.shape[1]  # fewer K/V heads than query heads: grouped-query attention
     specs = []
     for f in faults or []:
         specs.append(FaultSpec.parse(f) if isinstance(f, str) else f)
@@ -241,7 +244,7 @@ def efta_forward(q, k, v, mode="efta-opt", thr: Thresholds | None = None, faults
         debug = bool(specs) or observe_linear
     op = EftaAttention(b, h, s, d, mode=mode, thr=thr, scale=scale, observe_linear=observe_linear,
                        rowmax_bias=rowmax_bias, debug=debug, block=block, stride=stride,
-                       ev_cap=ev_cap, device=q.device)
+                       ev_cap=ev_cap, device=q.device, kv_heads=kv_heads)
     op.set_faults(specs)
     o, m, l = op(q4, k4, v4)
     rep = op.report(m.reshape(shape[:-1]), l.reshape(shape[:-1]))

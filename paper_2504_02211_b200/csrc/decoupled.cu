@@ -19,6 +19,7 @@
 //                                  checks (cols 128..131) — the reference's caug
 //   P_aug         [n*132, N]       fp16 normalised P, per tile followed by its column checksums
 //   V_aug         [N, d+8]         [V | s1_hi s2_hi s1_lo s2_lo | 0 0 0 0] (row checks of V)
+//   (grouped-query attention: K_aug / V_aug are built per query head from its group's K / V)
 //   O_aug         [n*132, d+8]     fp32 = P_aug V_aug
 // The GEMMs are plain library GEMMs (cuBLAS, fp16 in / fp32 out): the decoupled design is
 // "library GEMMs + separate checking kernels" by construction. The checking kernels
@@ -81,12 +82,20 @@ __device__ __noinline__ float dec_tap(const AttnParams& p, int head, int site, i
 // Q_aug / K_aug tiles: data rows copied, column checksums in fp32 ascending row order
 // (encode_traditional, src/abft.cpp:189-203; with_check_cols of K^T, decoupled.cpp:79-94, is the
 // same sum over the key rows), split hi/lo. grid (n, heads, 2 = {Q, K}), 128 threads.
+// K / V head of flat query head `head` (grouped-query attention; group 1 = itself)
+__device__ __forceinline__ int dec_kv_head(int head, int heads_q, int group) {
+    return group == 1 ? head : (head / heads_q) * (heads_q / group) + (head % heads_q) / group;
+}
+
+// q: this chunk's query heads; k: all K heads (row block of query head head0 + h's K/V head)
 __global__ void __launch_bounds__(128) dec_encode_qk_kernel(const __half* __restrict__ q,
                                                             const __half* __restrict__ k,
                                                             __half* __restrict__ qa, __half* __restrict__ ka,
-                                                            int N, int D, int n) {
+                                                            int N, int D, int n, int head0, int heads_q,
+                                                            int group) {
     const int i = blockIdx.x, h = blockIdx.y;
-    const __half* src = (blockIdx.z ? k : q) + (static_cast<size_t>(h) * N + static_cast<size_t>(i) * TB) * D;
+    const int src_head = blockIdx.z ? dec_kv_head(head0 + h, heads_q, group) : h;
+    const __half* src = (blockIdx.z ? k : q) + (static_cast<size_t>(src_head) * N + static_cast<size_t>(i) * TB) * D;
     __half* dst = (blockIdx.z ? ka : qa) + (static_cast<size_t>(h) * n + i) * TA * D;
     for (int idx = threadIdx.x; idx < TB * D / 8; idx += blockDim.x)
         reinterpret_cast<uint4*>(dst)[idx] = reinterpret_cast<const uint4*>(src)[idx];
@@ -108,10 +117,12 @@ __global__ void __launch_bounds__(128) dec_encode_qk_kernel(const __half* __rest
 // V_aug rows: [V | row checksums hi/lo | 0] (with_check_cols(v), decoupled.cpp:79-94: s1 = sum_c V,
 // s2 = sum_c (c+1) V in ascending column order). grid (n, heads), 128 threads = rows.
 __global__ void __launch_bounds__(128) dec_encode_v_kernel(const __half* __restrict__ v, __half* __restrict__ va,
-                                                           int N, int D, int DP) {
+                                                           int N, int D, int DP, int head0, int heads_q, int group) {
     const int i = blockIdx.x, h = blockIdx.y;
     const size_t row = static_cast<size_t>(h) * N + static_cast<size_t>(i) * TB + threadIdx.x;
-    const __half* src = v + row * D;
+    const size_t src_row = static_cast<size_t>(dec_kv_head(head0 + h, heads_q, group)) * N +
+                           static_cast<size_t>(i) * TB + threadIdx.x;
+    const __half* src = v + src_row * D;
     __half* dst = va + row * DP;
     float s1 = 0.0f, s2 = 0.0f;
     for (int c = 0; c < D; c += 8) {
@@ -896,8 +907,9 @@ std::string forward(const AttnParams& base, int bh, int N, int D, const __half* 
         const bool taps = dp.p.n_faults > 0;
         dp.s_aug = sa; dp.p_aug = pa; dp.o_aug = oa;
         // kernel 0: checksum-augmented operands
-        dec_encode_qk_kernel<<<dim3(n, nh, 2), 128, 0, st>>>(q + e0, k + e0, qa, ka, N, D, n);
-        dec_encode_v_kernel<<<dim3(n, nh), 128, 0, st>>>(v + e0, va, N, D, DP);
+        dec_encode_qk_kernel<<<dim3(n, nh, 2), 128, 0, st>>>(q + e0, k, qa, ka, N, D, n, h0, base.heads_q,
+                                                             base.kv_group);
+        dec_encode_v_kernel<<<dim3(n, nh), 128, 0, st>>>(v, va, N, D, DP, h0, base.heads_q, base.kv_group);
         // kernel 1: S_aug = Q_aug K_aug^T (row-major; column-major view: S^T = K_aug . Q_aug^T)
         cublasStatus_t cs = cublasGemmStridedBatchedEx(
             hd.h, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(ld), static_cast<int>(ld), D, &one, ka, CUDA_R_16F, D,

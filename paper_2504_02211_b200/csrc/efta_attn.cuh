@@ -63,8 +63,15 @@ struct AttnParams {
     float* scratch;  // workspace scratch: the persistent pair kernel's tile counter (int at [0])
     unsigned long long* prof;  // EFTA_PROF builds only: phase timestamps of one CTA
     const __half* q;           // [BH, S, D]: the pair kernel's rare path recomputes score c2 from Q . KC2
-    const __half* kc;          // [BH*n, 32, D] checksum rows (workspace)
+    const __half* kc;          // [BH_kv*n, 32, D] checksum rows (workspace)
+    int heads_q;               // query heads per batch entry (H)
+    int kv_group;              // query heads per K/V head (GQA; 1 = multi-head attention)
 };
+
+// Grouped-query attention: flat query head (b*H + h) -> flat K/V head (b*H_kv + h / group)
+__device__ __forceinline__ int kv_head(const AttnParams& p, int head) {
+    return p.kv_group == 1 ? head : (head / p.heads_q) * (p.heads_q / p.kv_group) + (head % p.heads_q) / p.kv_group;
+}
 
 #ifdef EFTA_PROF
 // phase timestamps (clock64) of CTA (2,5) (a pair leader): lane 0 of the stamping warp;

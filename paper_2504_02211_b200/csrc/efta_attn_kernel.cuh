@@ -27,7 +27,7 @@ template <int D>
 __device__ __noinline__ void pair_score_c2(const AttnParams& p, int head, int bi, int j, int row,
                                            float (&c2s)[kStride]) {
     const __half* qr = p.q + (static_cast<size_t>(head) * p.seq_len + static_cast<size_t>(bi) * kBlock + row) * D;
-    const __half* kc = p.kc + (static_cast<size_t>(head) * p.nblk + j) * 32 * D;
+    const __half* kc = p.kc + (static_cast<size_t>(kv_head(p, head)) * p.nblk + j) * 32 * D;
     for (int x = 0; x < kStride; ++x) {
         float acc = 0.0f;
         for (int k = 0; k < D; ++k) {
@@ -833,6 +833,7 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
     const int warp = warp_id(), lane = lane_id();
     const int qt = blockIdx.x, head = blockIdx.y, n = p.nblk;
     const int seq_row0 = head * p.seq_len;
+    const int kvh = kv_head(p, head), kv_row0 = kvh * p.seq_len;  // K / V / checksum operands (GQA)
 
     if (warp == 0 && lane == 0) {
         mbar_init(q_full, 1);
@@ -869,10 +870,10 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
 #pragma unroll
                 for (int sub = 0; sub < NSUB; ++sub) {
                     tma_load_2d(dst + sub * L::K_SUB, &tm_k, &k_full[s], sub * 64,
-                                seq_row0 + j * kBlock, kEvictLast);
+                                kv_row0 + j * kBlock, kEvictLast);
                     if (PROT)
                         tma_load_2d(dst + sub * L::K_SUB + 16384, &tm_kc, &k_full[s], sub * 64,
-                                    (head * n + j) * 32, kEvictLast);
+                                    (kvh * n + j) * 32, kEvictLast);
                 }
             }
         }
@@ -891,10 +892,10 @@ efta_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_cons
                 mbar_arrive_expect_tx(&v_full[s], L::V_BYTES + (PROT ? L::VC_BYTES : 0));
 #pragma unroll
                 for (int sub = 0; sub < NSUB; ++sub)
-                    tma_load_2d(dst + sub * 16384, &tm_v, &v_full[s], sub * 64, seq_row0 + j * kBlock,
+                    tma_load_2d(dst + sub * 16384, &tm_v, &v_full[s], sub * 64, kv_row0 + j * kBlock,
                                 kEvictLast);
                 if (PROT)
-                    tma_load_2d(dst + NSUB * 16384, &tm_vc, &v_full[s], 0, (head * n + j) * kBlock,
+                    tma_load_2d(dst + NSUB * 16384, &tm_vc, &v_full[s], 0, (kvh * n + j) * kBlock,
                                 kEvictLast);
             }
         }

@@ -266,14 +266,15 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                 const int u = pair_next_tile(tinfo, t_full, t_empty, k, false);
                 if (u < 0) break;
                 const int head = u / npq;
-                const int seq_row0 = head * p.seq_len;
+                const int kvh = kv_head(p, head);  // GQA: the K / checksum operands of the head's group
+                const int seq_row0 = kvh * p.seq_len;
                 for (int j = 0; j < n; ++j, ++g) {
                     const int s = g % KS;
                     mbar_wait(&k_empty[s], ((g / KS) & 1) ^ 1);
                     uint8_t* dst = smem + L::OFF_K + s * L::K_STAGE;
                     if (rank == 0) mbar_arrive_expect_tx(&k_full[s], 2 * L::K_STAGE);
                     const int krow = seq_row0 + j * kBlock;
-                    const int crow = (head * n + j) * 32;
+                    const int crow = (kvh * n + j) * 32;
 #pragma unroll
                     for (int sub = 0; sub < NSUB; ++sub) {
                         uint8_t* c = dst + sub * L::K_CHUNK;
@@ -341,7 +342,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                     mbar_wait(&v_empty[s], ((g / VS) & 1) ^ 1);
                     uint8_t* dst = smem + L::OFF_V + s * L::V_STAGE;
                     if (rank == 0) mbar_arrive_expect_tx(&v_full[s], 2 * L::V_STAGE);
-                    const int vrow = (head * n + j) * L::VROWS + L::HN_V * rank;
+                    const int vrow = (kv_head(p, head) * n + j) * L::VROWS + L::HN_V * rank;
 #pragma unroll
                     for (int c = 0; c < 2; ++c)
                         tma_load_2d_pair(dst + c * L::V_CHUNK, &tm_vt, &v_full[s], c * 64, vrow, kEvictLast);

@@ -92,6 +92,8 @@ int validate(const efta_attn_desc* d) {
     if (d->mode < EFTA_MODE_NONE || d->mode > EFTA_MODE_DECOUPLED) return fail(1, "efta_b200: unsupported mode");
     const long long bh = static_cast<long long>(d->batch) * d->heads;
     if (bh > 65535) return fail(1, "efta_b200: batch*heads must be <= 65535");
+    if (d->kv_heads < 0 || d->kv_heads > d->heads || (d->kv_heads > 0 && d->heads % d->kv_heads != 0))
+        return fail(1, "efta_b200: kv_heads must divide heads (grouped-query attention)");
     return 0;
 }
 
@@ -100,8 +102,10 @@ int validate(const efta_attn_desc* d) {
 struct WsLayout {
     size_t kc, r2, scratch, total;
 };
+int kv_heads_of(const efta_attn_desc* d) { return d->kv_heads > 0 ? d->kv_heads : d->heads; }
+
 WsLayout ws_layout(const efta_attn_desc* d) {
-    const size_t bh = static_cast<size_t>(d->batch) * d->heads;
+    const size_t bh = static_cast<size_t>(d->batch) * kv_heads_of(d);  // checksum operands per K/V head
     const size_t nblk = d->seq_len / kBlock;
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     WsLayout w;
@@ -130,7 +134,7 @@ bool use_pair(const efta_attn_desc* d) {
 
 int encode_kv(const efta_attn_desc* d, const void* k, const void* v, void* kc, void* vc,
               cudaStream_t st) {
-    const int bh = d->batch * d->heads, nblk = d->seq_len / kBlock;
+    const int bh = d->batch * kv_heads_of(d), nblk = d->seq_len / kBlock;
     dim3 grid(nblk, bh);
     if (d->head_dim == 64)
         efta_encode_kv_kernel<64><<<grid, 256, 0, st>>>(
@@ -191,6 +195,7 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
         return fail(1, "efta_attn_fwd_f16: fault injection needs the debug (tap) kernel variant");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int bh = d->batch * d->heads, nblk = d->seq_len / kBlock, D = d->head_dim;
+    const int bh_kv = d->batch * kv_heads_of(d);  // K / V heads (grouped-query attention)
     if (d->mode == EFTA_MODE_DECOUPLED) {
         // the decoupled baseline (src/decoupled.cpp:98-282): three kernels + cuBLAS GEMMs with
         // the N^2 intermediates in the workspace (csrc/decoupled.cu)
@@ -215,6 +220,8 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
         p.n_faults = faults ? n_faults : 0;
         p.fired = fired;
         p.fired_cap = fired ? fired_cap : 0;
+        p.heads_q = d->heads;
+        p.kv_group = d->heads / kv_heads_of(d);
         const std::string err = efta_dec::forward(p, bh, d->seq_len, D, reinterpret_cast<const __half*>(q),
                                                   reinterpret_cast<const __half*>(k),
                                                   reinterpret_cast<const __half*>(v), o, workspace, st);
@@ -233,22 +240,23 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     uint16_t* r2 = wsb ? reinterpret_cast<uint16_t*>(wsb + wl.r2) : nullptr;
     CUtensorMap tq, tk, tv, tkc, tvc;
     const uint64_t rows = static_cast<uint64_t>(bh) * d->seq_len;
+    const uint64_t kv_rows = static_cast<uint64_t>(bh_kv) * d->seq_len;
     bool ok;
     if (pair) {
         // prepass: KC (protected) + [V^T ; VC^T]; then maps for the half-operands
         if (!d->checksums_ready) {
-            cudaError_t e = D == 64 ? efta_launch_encode_pair_d64(prot, k, v, kc, r2, d->seq_len, nblk, bh, st)
-                                    : efta_launch_encode_pair_d128(prot, k, v, kc, r2, d->seq_len, nblk, bh, st);
+            cudaError_t e = D == 64 ? efta_launch_encode_pair_d64(prot, k, v, kc, r2, d->seq_len, nblk, bh_kv, st)
+                                    : efta_launch_encode_pair_d128(prot, k, v, kc, r2, d->seq_len, nblk, bh_kv, st);
             if (e != cudaSuccess) return fail(2, std::string("encode: ") + cudaGetErrorString(e));
         }
         const int vrows = prot ? D + 32 : D;
         // score operand N = 144 (protected: K + c1_hi + c1_lo rows) or 128, half per CTA:
         // leader K rows 0..71 (0..63), peer K rows 72..127 + two 8-row KC boxes (64..127)
-        ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, rows, D, prot ? 72 : 64) &&
-             make_map(&tvc, r2, static_cast<uint64_t>(bh) * nblk * vrows, 128, vrows / 2);
+        ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, kv_rows, D, prot ? 72 : 64) &&
+             make_map(&tvc, r2, static_cast<uint64_t>(bh_kv) * nblk * vrows, 128, vrows / 2);
         if (prot)
-            ok = ok && make_map(&tv, k, rows, D, 56) &&
-                 make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 8);
+            ok = ok && make_map(&tv, k, kv_rows, D, 56) &&
+                 make_map(&tkc, kc, static_cast<uint64_t>(bh_kv) * nblk * 32, D, 8);
         else {
             tv = tk;
             tkc = tk;
@@ -257,11 +265,11 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
         if (prot && !d->checksums_ready) {
             if (int rc = encode_kv(d, k, v, kc, r2, st)) return rc;
         }
-        ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, rows, D, 128) &&
-             make_map(&tv, v, rows, D, 128);
+        ok = make_map(&tq, q, rows, D, 128) && make_map(&tk, k, kv_rows, D, 128) &&
+             make_map(&tv, v, kv_rows, D, 128);
         if (prot) {
-            ok = ok && make_map(&tkc, kc, static_cast<uint64_t>(bh) * nblk * 32, D, 32) &&
-                 make_map(&tvc, r2, static_cast<uint64_t>(bh) * nblk * 128, 64, 128);
+            ok = ok && make_map(&tkc, kc, static_cast<uint64_t>(bh_kv) * nblk * 32, D, 32) &&
+                 make_map(&tvc, r2, static_cast<uint64_t>(bh_kv) * nblk * 128, 64, 128);
         } else {
             tkc = tq;
             tvc = tq;
@@ -304,6 +312,8 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     p.scratch = wsb ? reinterpret_cast<float*>(wsb + wl.scratch) : nullptr;
     p.q = reinterpret_cast<const __half*>(q);
     p.kc = reinterpret_cast<const __half*>(kc);
+    p.heads_q = d->heads;
+    p.kv_group = d->heads / kv_heads_of(d);
     const bool dbg = d->debug != 0;
     cudaError_t e;
     if (pair)  // the persistent pair kernel's in-order tile counter (workspace scratch, int)
@@ -332,8 +342,13 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
     // (separate copy engines; PCIe is full duplex). Fault-injection calls (head-indexed
     // fault tables, fired lists) run as one chunk.
     const int bh = d->batch * d->heads;
-    const int nchunk = (n_faults > 0 || fired) ? 1 : std::min(bh, 32);  // small first-H2D / last-D2H tails
-    const int per = (bh + nchunk - 1) / nchunk;
+    // chunk unit: one head, or one batch entry (all its query heads and their K/V group heads)
+    // under grouped-query attention
+    const bool gqa = kv_heads_of(d) != d->heads;
+    const int units = gqa ? d->batch : bh;
+    const int qh_unit = gqa ? d->heads : 1, kvh_unit = gqa ? kv_heads_of(d) : 1;
+    const int nchunk = (n_faults > 0 || fired) ? 1 : std::min(units, 32);  // small first-H2D / last-D2H tails
+    const int per = (units + nchunk - 1) / nchunk;
     struct Scratch {
         void* p = nullptr;
         size_t n = 0;
@@ -357,13 +372,20 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
     }
     const size_t head_elems = static_cast<size_t>(d->seq_len) * d->head_dim;
     const size_t n_in = static_cast<size_t>(bh) * head_elems;
-    const size_t bytes_in = n_in * 2, bytes_o = n_in * 4, bytes_ml = static_cast<size_t>(bh) * d->seq_len * 4;
-    efta_attn_desc dc = *d;  // one chunk: batch 1 x `per` heads
-    dc.batch = 1;
-    dc.heads = per;
+    const size_t n_kv = static_cast<size_t>(d->batch) * kv_heads_of(d) * head_elems;
+    const size_t bytes_in = n_in * 2, bytes_kv = n_kv * 2, bytes_o = n_in * 4,
+                 bytes_ml = static_cast<size_t>(bh) * d->seq_len * 4;
+    efta_attn_desc dc = *d;  // one chunk: `per` units
+    if (gqa) {
+        dc.batch = per;
+    } else {
+        dc.batch = 1;
+        dc.heads = per;
+        dc.kv_heads = 0;
+    }
     const size_t wsb = ws_bytes(&dc);
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    const size_t need = 3 * al(bytes_in) + al(bytes_o) + 2 * al(bytes_ml) + al(wsb) +
+    const size_t need = al(bytes_in) + 2 * al(bytes_kv) + al(bytes_o) + 2 * al(bytes_ml) + al(wsb) +
                         nchunk * al(sizeof(efta_counters)) + al(sizeof(efta_fault_spec) * (n_faults + 1)) +
                         nchunk * al(sizeof(efta_event) * (ev_cap + 1)) + al(sizeof(efta_fired) * (fired_cap + 1));
     if (s.n < need) {
@@ -376,8 +398,8 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
     char* base = static_cast<char*>(s.p);
     auto take = [&](size_t b) { char* r = base; base += al(b); return r; };
     uint16_t* dq = reinterpret_cast<uint16_t*>(take(bytes_in));
-    uint16_t* dk = reinterpret_cast<uint16_t*>(take(bytes_in));
-    uint16_t* dv = reinterpret_cast<uint16_t*>(take(bytes_in));
+    uint16_t* dk = reinterpret_cast<uint16_t*>(take(bytes_kv));
+    uint16_t* dv = reinterpret_cast<uint16_t*>(take(bytes_kv));
     float* dout = reinterpret_cast<float*>(take(bytes_o));
     float* dm = reinterpret_cast<float*>(take(bytes_ml));
     float* dl = reinterpret_cast<float*>(take(bytes_ml));
@@ -391,21 +413,32 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
     if (n_faults > 0)
         CUDA_TRY(cudaMemcpyAsync(df, faults, sizeof(efta_fault_spec) * n_faults, cudaMemcpyHostToDevice, h2d));
     for (int c = 0; c < nchunk; ++c) {
-        const int h0 = c * per, nh = std::min(per, bh - h0);
-        if (nh <= 0) break;
+        const int u0 = c * per, nu = std::min(per, units - u0);
+        if (nu <= 0) break;
+        const int h0 = u0 * qh_unit, nh = nu * qh_unit;
         const size_t e0 = static_cast<size_t>(h0) * head_elems, ne = static_cast<size_t>(nh) * head_elems;
+        const size_t k0 = static_cast<size_t>(u0) * kvh_unit * head_elems,
+                     nk = static_cast<size_t>(nu) * kvh_unit * head_elems;
         const size_t r0 = static_cast<size_t>(h0) * d->seq_len, nr = static_cast<size_t>(nh) * d->seq_len;
         CUDA_TRY(cudaMemcpyAsync(dq + e0, q + e0, ne * 2, cudaMemcpyHostToDevice, h2d));
-        CUDA_TRY(cudaMemcpyAsync(dk + e0, k + e0, ne * 2, cudaMemcpyHostToDevice, h2d));
-        CUDA_TRY(cudaMemcpyAsync(dv + e0, v + e0, ne * 2, cudaMemcpyHostToDevice, h2d));
+        CUDA_TRY(cudaMemcpyAsync(dk + k0, k + k0, nk * 2, cudaMemcpyHostToDevice, h2d));
+        CUDA_TRY(cudaMemcpyAsync(dv + k0, v + k0, nk * 2, cudaMemcpyHostToDevice, h2d));
         CUDA_TRY(cudaEventRecord(s.ev[2 * c], h2d));
         CUDA_TRY(cudaStreamWaitEvent(comp, s.ev[2 * c], 0));
         efta_attn_desc dcc = *d;
-        if (nchunk > 1) { dcc.batch = 1; dcc.heads = nh; }
+        if (nchunk > 1) {
+            if (gqa) {
+                dcc.batch = nu;
+            } else {
+                dcc.batch = 1;
+                dcc.heads = nh;
+                dcc.kv_heads = 0;
+            }
+        }
         dcc.checksums_ready = 0;  // the internal workspace never holds this call's operands
         efta_counters* cc = reinterpret_cast<efta_counters*>(reinterpret_cast<char*>(dcnt) + c * cnt_stride);
         efta_event* ce = reinterpret_cast<efta_event*>(reinterpret_cast<char*>(de) + c * ev_stride);
-        int rc = efta_attn_fwd_f16(&dcc, dq + e0, dk + e0, dv + e0, dout + e0, dm + r0, dl + r0, dws, wsb,
+        int rc = efta_attn_fwd_f16(&dcc, dq + e0, dk + k0, dv + k0, dout + e0, dm + r0, dl + r0, dws, wsb,
                                    n_faults > 0 ? df : nullptr, n_faults, events ? ce : nullptr,
                                    events ? ev_cap : 0, fired ? dfi : nullptr, fired ? fired_cap : 0, cc, comp);
         if (rc) return rc;
@@ -437,7 +470,7 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
             if (take_n > 0) {
                 const char* src = reinterpret_cast<const char*>(de) + c * ev_stride;
                 CUDA_TRY(cudaMemcpy(events + n_ev, src, sizeof(efta_event) * take_n, cudaMemcpyDeviceToHost));
-                for (int i = 0; i < take_n; ++i) events[n_ev + i].head += c * per;
+                for (int i = 0; i < take_n; ++i) events[n_ev + i].head += c * per * qh_unit;
                 n_ev += take_n;
             }
         }

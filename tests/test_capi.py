@@ -34,7 +34,7 @@ def _desc(**kw):
     from paper_2504_02211_b200 import _lib
     d = dict(batch=1, heads=12, seq_len=512, head_dim=64, block=128, stride=8, scale=0.0, mode=2,
              eps1=7e-6, eps2=0.48, eps_lin=0.48, observe_linear=0, rowmax_bias=0.0, debug=0,
-             checksums_ready=0)
+             checksums_ready=0, kv_heads=0)
     d.update(kw)
     return _lib.AttnDesc(**d)
 
@@ -48,6 +48,8 @@ def _desc(**kw):
     (dict(head_dim=96), False, "head_dim must be 64 or 128"),
     (dict(mode=3), True, ""),                                  # DECOUPLED baseline (csrc/decoupled.cu)
     (dict(mode=4), False, "unsupported mode"),
+    (dict(kv_heads=4), True, ""),                              # grouped-query attention (F4)
+    (dict(kv_heads=5), False, "kv_heads must divide heads"),
 ])
 def test_validate_mirrors_attnconfig(kw, ok, msg):
     from paper_2504_02211_b200 import _lib
@@ -146,3 +148,12 @@ def test_decoupled_workspace_is_chunked():
     per_head = (64 * 132) ** 2 * 4  # S_aug alone
     assert ws1 > per_head
     assert ws2 <= (4 << 30) + 256 and ws2 >= ws1
+
+
+def test_gqa_workspace_scales_with_kv_heads():
+    """Under grouped-query attention the checksum operands (KC, [V^T ; VC^T]) exist once per K/V
+    head: the workspace shrinks with the group size."""
+    from paper_2504_02211_b200 import _lib
+    mha = _lib.lib.efta_attn_workspace_bytes(C.byref(_desc(batch=2, heads=8, seq_len=1024)))
+    gqa = _lib.lib.efta_attn_workspace_bytes(C.byref(_desc(batch=2, heads=8, seq_len=1024, kv_heads=2)))
+    assert 0 < gqa < mha and abs(mha / gqa - 4.0) < 0.05
