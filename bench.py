@@ -33,7 +33,7 @@ B, H, S, D = 32, 32, 8192, 128
 BLOCK, STRIDE = 128, 8
 METRIC = "EFTA attention TFLOPS/GPU (EFTA-optimized fused forward)"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r01_attn_c4_traffic.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r02", "attn_c4_traffic.json")
 
 
 def flops(b, h, s, d):
