@@ -26,7 +26,9 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/efta_b200.h"
@@ -37,22 +39,29 @@ using namespace efta_sm100;
 
 namespace {
 
-constexpr int GM = 128, GN = 256, GK = 64;   // tile and k-chunk
+constexpr int GM = 128, GN = 256, GK = 64;   // tile (per CTA) and k-chunk
 #ifndef ABFT_STAGES
 #define ABFT_STAGES 3
 #endif
-constexpr int STAGES = ABFT_STAGES;  // 3 x 52 KB (+ the epilogue staging buffers); 4 stages left no room for them
-constexpr uint32_t A_BYTES = GM * GK * 2;            // 16 KB
-constexpr uint32_t B_HALF = (128 + 16) * GK * 2;     // 18 KB: 128 W rows + 16 checksum rows
-constexpr uint32_t B_BYTES = 2 * B_HALF;             // 36 KB
-constexpr uint32_t STAGE = A_BYTES + B_BYTES;
-constexpr uint32_t OFF_BAR = STAGES * STAGE;
-constexpr uint32_t OFF_TMEM = OFF_BAR + (2 * STAGES + 2) * 8;
-constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
-constexpr uint32_t OFF_XS = OFF_RED + 128 * 24 + 256;  // column half 1's partial strided sums [128][16]
-constexpr uint32_t OFF_STG = (OFF_XS + 128 * 16 * 4 + 16 + 127) & ~127u;  // epilogue staging: 8 warps x 4 KB
-constexpr uint32_t SMEM_BYTES = OFF_STG + 8 * 4096 + 1024;
-static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+// PAIR: a cluster of two CTAs (cta_group::2) computes a 256 x 256 tile; each CTA holds its 128
+// rows of X and HALF of each B operand (72 of the 144 rows of [W rows | checksum rows] per MMA),
+// so a stage is 16 + 18 KB instead of 16 + 36 KB and five stages fit next to the staging buffers.
+template <bool PAIR>
+struct GemmLayout {
+    static constexpr int STAGES = PAIR ? 5 : ABFT_STAGES;
+    static constexpr uint32_t A_BYTES = GM * GK * 2;                  // 16 KB
+    static constexpr uint32_t B_HALF = (PAIR ? 72 : 144) * GK * 2;    // rows of one MMA's B operand
+    static constexpr uint32_t B_BYTES = 2 * B_HALF;
+    static constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+    static constexpr uint32_t OFF_BAR = STAGES * STAGE;
+    static constexpr uint32_t OFF_TMEM = OFF_BAR + (2 * STAGES + 2) * 8;
+    static constexpr uint32_t OFF_RED = (OFF_TMEM + 16 + 15) & ~15u;
+    static constexpr uint32_t OFF_XS = OFF_RED + 128 * 24 + 256;  // column half 1's partial strided sums [128][16]
+    static constexpr uint32_t OFF_STG = (OFF_XS + 128 * 16 * 4 + 16 + 127) & ~127u;  // staging: 8 warps x 4 KB
+    static constexpr uint32_t SMEM_BYTES = OFF_STG + 8 * 4096 + 1024;
+    static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+    static_assert(B_HALF % 1024 == 0 && A_BYTES % 1024 == 0, "swizzle atoms stay 1 KB aligned");
+};
 constexpr int GEMM_THREADS = 384;  // warps 0-3: TMA / MMA / idle / idle; 4-11: epilogue (2 column halves)
 
 struct GemmParams {
@@ -73,52 +82,98 @@ struct RowScratchG {
     double* dbl;
 };
 
-template <bool DBG, bool F32>
+// tm_w: W rows in boxes of 128 (single CTA) or 72 (pair); tm_wb: boxes of 56 (pair, the peer's
+// W rows next to its 16 checksum rows); tm_wc: checksum rows in boxes of 16.
+template <bool DBG, bool F32, bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
-                 const __grid_constant__ CUtensorMap tm_wc, const GemmParams p) {
+                 const __grid_constant__ CUtensorMap tm_wb, const __grid_constant__ CUtensorMap tm_wc,
+                 const GemmParams p) {
+    using L = GemmLayout<PAIR>;
+    constexpr int STAGES = L::STAGES;
+    constexpr uint32_t A_BYTES = L::A_BYTES, B_HALF = L::B_HALF, STAGE = L::STAGE;
+    constexpr uint32_t OFF_RED = L::OFF_RED, OFF_XS = L::OFF_XS, OFF_STG = L::OFF_STG;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
     const int warp = warp_id(), lane = lane_id();
-    const int n_tiles_total = p.m_tiles * p.n_tiles;
+    const uint32_t rank = PAIR ? cluster_rank() : 0u;
+    // tiles: 128 x 256 per CTA, or 256 x 256 per CTA pair (this CTA: rows rank*128 .. +127)
+    const int m_units = PAIR ? p.m_tiles / 2 : p.m_tiles;
+    const int n_tiles_total = m_units * p.n_tiles;
+    const int t0 = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int t_step = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         mbar_init(tfull, 1);
-        mbar_init(tempty, 256);
+        mbar_init(tempty, PAIR ? 16 : 256);  // pair: one arrival per epilogue warp of both CTAs (leader)
         fence_barrier_init();
         tma_prefetch_desc(&tm_x);
         tma_prefetch_desc(&tm_w);
         tma_prefetch_desc(&tm_wc);
+        if (PAIR) tma_prefetch_desc(&tm_wb);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    if (warp == 1) {
+        if (PAIR) tmem_alloc2(tmem_slot, 512);
+        else tmem_alloc(tmem_slot, 512);
+    }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();  // both CTAs' barriers exist before any remote arrive / TMA
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // the accumulator is drained: the (leader's) MMA issuer may overwrite it
+    auto release_acc = [&]() {
+        tc_fence_before();
+        if constexpr (PAIR) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty, 0);
+        } else {
+            mbar_arrive(tempty);
+        }
+    };
 
     if (warp == 0) {
         setmaxnreg_dec<40>();
         if (lane == 0) {  // ------------------------------------------ TMA producer
             int it = 0;
-            for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+            for (int t = t0; t < n_tiles_total; t += t_step) {
                 const int mt = t / p.n_tiles, nt = t % p.n_tiles;
                 for (int kc = 0; kc < p.k_chunks; ++kc, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     uint8_t* a = smem + s * STAGE;
                     uint8_t* b = a + A_BYTES;
-                    mbar_arrive_expect_tx(&full[s], STAGE);
-                    tma_load_2d(a, &tm_x, &full[s], kc * GK, mt * GM, kEvictNormal);
-                    tma_load_2d(b, &tm_w, &full[s], kc * GK, nt * GN, kEvictLast);
-                    tma_load_2d(b + 16384, &tm_wc, &full[s], kc * GK, nt * 32, kEvictLast);
-                    tma_load_2d(b + B_HALF, &tm_w, &full[s], kc * GK, nt * GN + 128, kEvictLast);
-                    tma_load_2d(b + B_HALF + 16384, &tm_wc, &full[s], kc * GK, nt * 32 + 16, kEvictLast);
+                    if constexpr (PAIR) {
+                        // both CTAs' bytes land on the leader's barrier; B halves as in the
+                        // attention pair kernel: rank 0 = W rows 0..71 of each MMA's operand,
+                        // rank 1 = W rows 72..127 + that MMA's 16 checksum rows
+                        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE);
+                        tma_load_2d_pair(a, &tm_x, &full[s], kc * GK, mt * 2 * GM + rank * GM, kEvictNormal);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            uint8_t* bh = b + h * B_HALF;
+                            if (rank == 0) {
+                                tma_load_2d_pair(bh, &tm_w, &full[s], kc * GK, nt * GN + h * 128, kEvictLast);
+                            } else {
+                                tma_load_2d_pair(bh, &tm_wb, &full[s], kc * GK, nt * GN + h * 128 + 72, kEvictLast);
+                                tma_load_2d_pair(bh + 56 * 128, &tm_wc, &full[s], kc * GK, nt * 32 + h * 16,
+                                                 kEvictLast);
+                            }
+                        }
+                    } else {
+                        mbar_arrive_expect_tx(&full[s], STAGE);
+                        tma_load_2d(a, &tm_x, &full[s], kc * GK, mt * GM, kEvictNormal);
+                        tma_load_2d(b, &tm_w, &full[s], kc * GK, nt * GN, kEvictLast);
+                        tma_load_2d(b + 16384, &tm_wc, &full[s], kc * GK, nt * 32, kEvictLast);
+                        tma_load_2d(b + B_HALF, &tm_w, &full[s], kc * GK, nt * GN + 128, kEvictLast);
+                        tma_load_2d(b + B_HALF + 16384, &tm_wc, &full[s], kc * GK, nt * 32 + 16, kEvictLast);
+                    }
                 }
             }
         }
@@ -126,31 +181,41 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
         // ------------------------------------------------------------- MMA issuer
         // converged warp, one elected lane issues (descriptors stay in uniform registers)
         setmaxnreg_dec<40>();
-        constexpr uint32_t ID = idesc_f16_f32(128, 144, 0, 0);
+        constexpr uint32_t ID = idesc_f16_f32(PAIR ? 256 : 128, 144, 0, 0);
         const uint64_t d0 = smem_desc_sw128(smem_u32(smem), 16, 1024);
         int it = 0, tl = 0;
-        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
-            mbar_wait(tempty, (tl & 1) ^ 1);  // epilogue drained the accumulator
-            tc_fence_after();
-            for (int kc = 0; kc < p.k_chunks; ++kc, ++it) {
-                const int s = it % STAGES;
-                mbar_wait(&full[s], (it / STAGES) & 1);
+        if (!PAIR || rank == 0)  // the pair leader issues for both CTAs
+            for (int t = t0; t < n_tiles_total; t += t_step, ++tl) {
+                mbar_wait(tempty, (tl & 1) ^ 1);  // the epilogue(s) drained the accumulator
                 tc_fence_after();
-                const uint64_t ad = d0 + ((s * STAGE) >> 4), bd = ad + (A_BYTES >> 4);
-                if (elect_one()) {
+                for (int kc = 0; kc < p.k_chunks; ++kc, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint64_t ad = d0 + ((s * STAGE) >> 4), bd = ad + (A_BYTES >> 4);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < GK / 16; ++kk) {
-                        const uint32_t acc = (kc | kk) > 0;
-                        mma_ss(tmem, ad + kk * 2, bd + kk * 2, ID, acc);
-                        mma_ss(tmem + 144, ad + kk * 2, bd + (B_HALF >> 4) + kk * 2, ID, acc);
+                        for (int kk = 0; kk < GK / 16; ++kk) {
+                            const uint32_t acc = (kc | kk) > 0;
+                            if constexpr (PAIR) {
+                                mma2_ss(tmem, ad + kk * 2, bd + kk * 2, ID, acc);
+                                mma2_ss(tmem + 144, ad + kk * 2, bd + (B_HALF >> 4) + kk * 2, ID, acc);
+                            } else {
+                                mma_ss(tmem, ad + kk * 2, bd + kk * 2, ID, acc);
+                                mma_ss(tmem + 144, ad + kk * 2, bd + (B_HALF >> 4) + kk * 2, ID, acc);
+                            }
+                        }
+                        if constexpr (PAIR) commit2_both(&empty[s]);
+                        else tc_commit(&empty[s]);
                     }
-                    tc_commit(&empty[s]);
+                    __syncwarp();
+                }
+                if (elect_one()) {
+                    if constexpr (PAIR) commit2_both(tfull);
+                    else tc_commit(tfull);
                 }
                 __syncwarp();
             }
-            if (elect_one()) tc_commit(tfull);
-            __syncwarp();
-        }
     } else if (warp < 4) {
         setmaxnreg_dec<40>();
     } else {
@@ -166,8 +231,9 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
         int* dec = reinterpret_cast<int*>(smem + OFF_XS + 128 * 16 * 4);  // the lower half's tile verdict
         float fam = 0.0f;
         int tl = 0;
-        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tl) {
-            const int mt = t / p.n_tiles, nt = t % p.n_tiles;
+        for (int t = t0; t < n_tiles_total; t += t_step, ++tl) {
+            const int nt = t % p.n_tiles;
+            const int mt = PAIR ? (t / p.n_tiles) * 2 + static_cast<int>(rank) : t / p.n_tiles;  // 128-row block
             const int grow = mt * GM + row;
             // this row's injected upset, if any (global coordinates)
             int f_col = -1, f_bit = 0;
@@ -253,15 +319,11 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                 named_bar_arrive(6, 256);
                 named_bar_sync(7, 256);
                 const bool rare = *reinterpret_cast<volatile int*>(dec) != 0;
-                if (!rare) {
-                    tc_fence_before();
-                    mbar_arrive(tempty);
-                }
+                if (!rare) release_acc();
                 store_half();
                 if (rare) {
                     named_bar_arrive(8, 256);  // raw values stored before the lower half corrects
-                    tc_fence_before();
-                    mbar_arrive(tempty);
+                    release_acc();
                 }
                 continue;
             }
@@ -302,8 +364,7 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
             if (row == 0) *dec = any ? 1 : 0;
             named_bar_arrive(7, 256);
             if (!any) {
-                tc_fence_before();
-                mbar_arrive(tempty);
+                release_acc();
                 store_half();
                 continue;
             }
@@ -362,8 +423,7 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                     }
                 }
             }
-            tc_fence_before();
-            mbar_arrive(tempty);
+            release_acc();
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) fam = fmaxf(fam, __shfl_xor_sync(0xffffffffu, fam, off));
@@ -371,8 +431,12 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();  // the peer's MMAs / remote arrivals are done
     tc_fence_after();
-    if (warp == 1) tmem_dealloc(tmem, 512);
+    if (warp == 1) {
+        if (PAIR) tmem_dealloc2(tmem, 512);
+        else tmem_dealloc(tmem, 512);
+    }
 }
 
 // weight checksum rows: Wc[t][32][K] from W[N][K] over each 256-wide output tile
@@ -466,8 +530,12 @@ int efta_abft_gemm_ex(const efta_gemm_desc* d, const uint16_t* x, const uint16_t
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(efta_counters), st);
     if (e != cudaSuccess) return gfail(2, cudaGetErrorString(e));
-    CUtensorMap tx, tw, twc;
-    if (!gmap(&tx, x, d->m, d->k, 128) || !gmap(&tw, w, d->n, d->k, 128) ||
+    // CTA pairs (M = 256 per cluster) whenever the rows split into 256-row tiles; EFTA_GEMM_SINGLE=1
+    // forces the single-CTA kernel (A/B)
+    const bool pair = (d->m % (2 * GM)) == 0 && std::getenv("EFTA_GEMM_SINGLE") == nullptr;
+    CUtensorMap tx, tw, twb, twc;
+    if (!gmap(&tx, x, d->m, d->k, 128) || !gmap(&tw, w, d->n, d->k, pair ? 72 : 128) ||
+        !gmap(&twb, w, d->n, d->k, pair ? 56 : 128) ||
         !gmap(&twc, wcs, static_cast<uint64_t>(d->n / GN) * 32, d->k, 16))
         return gfail(2, "abft_gemm: cuTensorMapEncodeTiled failed");
     GemmParams p{};
@@ -488,18 +556,37 @@ int efta_abft_gemm_ex(const efta_gemm_desc* d, const uint16_t* x, const uint16_t
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int tiles = p.m_tiles * p.n_tiles;
-    const int grid = tiles < nsm ? tiles : nsm;
-    auto launch = [&](auto kern) -> cudaError_t {
-        cudaError_t ee = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    auto launch = [&](auto kern, bool is_pair) -> cudaError_t {
+        const uint32_t smem_bytes = is_pair ? GemmLayout<true>::SMEM_BYTES : GemmLayout<false>::SMEM_BYTES;
+        cudaError_t ee = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
         if (ee != cudaSuccess) return ee;
-        kern<<<grid, GEMM_THREADS, SMEM_BYTES, st>>>(tx, tw, twc, p);
-        return cudaGetLastError();
+        const int tiles = is_pair ? (p.m_tiles / 2) * p.n_tiles : p.m_tiles * p.n_tiles;
+        const int units = is_pair ? std::min(tiles, std::max(1, nsm / 2)) : std::min(tiles, nsm);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(is_pair ? 2 * units : units);
+        cfg.blockDim = dim3(GEMM_THREADS);
+        cfg.dynamicSmemBytes = smem_bytes;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = is_pair ? 2 : 1;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, tx, tw, twb, twc, p);
     };
-    if (y_f32)
-        e = d->debug ? launch(abft_gemm_kernel<true, true>) : launch(abft_gemm_kernel<false, true>);
-    else
-        e = d->debug ? launch(abft_gemm_kernel<true, false>) : launch(abft_gemm_kernel<false, false>);
+    if (pair) {
+        if (y_f32)
+            e = d->debug ? launch(abft_gemm_kernel<true, true, true>, true) : launch(abft_gemm_kernel<false, true, true>, true);
+        else
+            e = d->debug ? launch(abft_gemm_kernel<true, false, true>, true) : launch(abft_gemm_kernel<false, false, true>, true);
+    } else {
+        if (y_f32)
+            e = d->debug ? launch(abft_gemm_kernel<true, true, false>, false) : launch(abft_gemm_kernel<false, true, false>, false);
+        else
+            e = d->debug ? launch(abft_gemm_kernel<true, false, false>, false) : launch(abft_gemm_kernel<false, false, false>, false);
+    }
     return e == cudaSuccess ? 0 : gfail(2, cudaGetErrorString(e));
 }
 

@@ -78,3 +78,27 @@ def test_fault_located_and_corrected_like_oracle(problem, bit):
         if ro["status"] == "corrected":
             assert abs(y[r, c] - y0[r, c]) <= 1e-2 * max(1.0, abs(y0[r, c]))
     assert not rep.failed or any(e["status"] != "corrected" for e in rep.events)
+
+
+@pytest.mark.parametrize("m", [384, 512])
+def test_pair_and_single_cta_kernels_agree(m, monkeypatch):
+    """Rows split in 256-row tiles run on CTA pairs (cta_group::2, half of each B operand per CTA);
+    other row counts (and EFTA_GEMM_SINGLE=1) on single CTAs. Same sums in the same order: the
+    two kernels' fp32 products and tile checksums are bit-identical; a fault is located at the
+    same cell."""
+    import torch
+    from paper_2504_02211_b200.ffn import AbftLinear
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    x = torch.empty(m, 512, device="cuda").uniform_(-1, 1, generator=g).half()
+    w = (torch.empty(512, 512, device="cuda").uniform_(-1, 1, generator=g) / 512 ** 0.5).half()
+    outs = []
+    for single in ("0", "1"):
+        if single == "1":
+            monkeypatch.setenv("EFTA_GEMM_SINGLE", "1")
+        lin = AbftLinear(w, eps=EPS)
+        y = lin(x)
+        torch.cuda.synchronize()
+        outs.append((y.float().cpu().numpy(), lin.report().detections))
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert outs[0][1] == outs[1][1] == 0
