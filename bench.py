@@ -296,6 +296,22 @@ def suite(dev):
         dec.append(row)
         del q, k, v
     out["decoupled_vs_efta_opt"] = dec
+    # causal (decoder) attention on the pair kernel, a non-goal of the reference (F4):
+    # useful work = half of the square, 2*B*H*S^2*d FLOPs
+    cz = {}
+    b, h, s_, d = 4, 32, 8192, 128
+    q = synth_inputs(41, (b, h, s_, d), dev)
+    k = synth_inputs(42, (b, h, s_, d), dev)
+    v = synth_inputs(43, (b, h, s_, d), dev)
+    for mode in ("efta-opt", "none"):
+        op = EftaAttention(b, h, s_, d, mode=mode, thr=thr, device=dev, causal=True)
+        ms = _time_cuda(lambda: op(q, k, v), iters=3)
+        cz[f"causal_{mode}_tflops"] = round(flops(b, h, s_, d) / 2 / (ms * 1e-3) / 1e12, 2)
+        cz[f"causal_{mode}_detections"] = op.report().detections
+        del op
+    cz["shape"] = {"batch": b, "heads": h, "seq_len": s_, "head_dim": d}
+    out["causal"] = cz
+    del q, k, v
     return out
 
 

@@ -62,6 +62,10 @@ typedef struct {
                            0 (or heads) = multi-head attention. Not a reference feature (SPEC.md:141,
                            356 list GQA as a non-goal): each query head still runs the reference
                            algorithm on its group's K and V. */
+    int causal;         /* 1: key k is visible to query q only if k <= q (decoder self-attention).
+                           Not a reference feature: modes NONE / EFTA_OPTIMIZED on the CTA-pair
+                           kernel (even seq_len / 128), no fault-tap build. The diagonal block's
+                           exp-stage check runs on each group's visible cells. */
 } efta_attn_desc;
 
 const char* efta_last_error(void);

@@ -26,7 +26,7 @@ class AttnDesc(C.Structure):
                 ("scale", C.c_float), ("mode", C.c_int), ("eps1", C.c_double),
                 ("eps2", C.c_double), ("eps_lin", C.c_double), ("observe_linear", C.c_int),
                 ("rowmax_bias", C.c_float), ("debug", C.c_int), ("checksums_ready", C.c_int),
-                ("kv_heads", C.c_int)]
+                ("kv_heads", C.c_int), ("causal", C.c_int)]
 
 
 class FaultSpec(C.Structure):

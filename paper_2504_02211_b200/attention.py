@@ -122,10 +122,11 @@ class FTReport:
         return max(v) if v else -INF
 
 
-def _desc(b, h, s, d, mode, thr, scale, observe_linear, rowmax_bias, debug, block, stride, kv_heads=0):
+def _desc(b, h, s, d, mode, thr, scale, observe_linear, rowmax_bias, debug, block, stride, kv_heads=0,
+          causal=False):
     return _lib.AttnDesc(b, h, s, d, block, stride, float(scale), MODES[mode], float(thr.eps1),
                          float(thr.eps2), float(thr.eps_lin), 1 if observe_linear else 0,
-                         float(rowmax_bias), 1 if debug else 0, 0, int(kv_heads))
+                         float(rowmax_bias), 1 if debug else 0, 0, int(kv_heads), 1 if causal else 0)
 
 
 def _as_bhsd(x: torch.Tensor):
@@ -143,14 +144,14 @@ class EftaAttention:
 
     def __init__(self, batch, heads, seq_len, head_dim, mode="efta-opt", thr=None, scale=0.0,
                  observe_linear=False, rowmax_bias=0.0, debug=False, block=128, stride=8,
-                 ev_cap=4096, fired_cap=256, device="cuda", kv_heads=None):
+                 ev_cap=4096, fired_cap=256, device="cuda", kv_heads=None, causal=False):
         self.shape = (batch, heads, seq_len, head_dim)
         # grouped-query attention: K / V carry kv_heads heads (query head h reads h // group)
         self.kv_heads = heads if not kv_heads else int(kv_heads)
         self.mode = mode
         self.thr = thr or Thresholds()
         self.desc = _desc(batch, heads, seq_len, head_dim, mode, self.thr, scale, observe_linear,
-                          rowmax_bias, debug, block, stride, self.kv_heads)
+                          rowmax_bias, debug, block, stride, self.kv_heads, causal)
         check(lib.efta_attn_validate(C.byref(self.desc)))
         ws = lib.efta_attn_workspace_bytes(C.byref(self.desc))
         dev = torch.device(device)
@@ -228,7 +229,7 @@ class EftaAttention:
 
 def efta_forward(q, k, v, mode="efta-opt", thr: Thresholds | None = None, faults=None,
                  scale=0.0, observe_linear=False, rowmax_bias=0.0, debug=None, block=128,
-                 stride=8, ev_cap=4096):
+                 stride=8, ev_cap=4096, causal=False):
     """One protected (or plain) attention forward. q/k/v: CUDA fp16 [S,d], [BH,S,d]
     or [B,H,S,d]. Returns (O fp32 with q's shape, FTReport)."""
     shape = q.shape
@@ -244,7 +245,7 @@ def efta_forward(q, k, v, mode="efta-opt", thr: Thresholds | None = None, faults
         debug = bool(specs) or observe_linear
     op = EftaAttention(b, h, s, d, mode=mode, thr=thr, scale=scale, observe_linear=observe_linear,
                        rowmax_bias=rowmax_bias, debug=debug, block=block, stride=stride,
-                       ev_cap=ev_cap, device=q.device, kv_heads=kv_heads)
+                       ev_cap=ev_cap, device=q.device, kv_heads=kv_heads, causal=causal)
     op.set_faults(specs)
     o, m, l = op(q4, k4, v4)
     rep = op.report(m.reshape(shape[:-1]), l.reshape(shape[:-1]))

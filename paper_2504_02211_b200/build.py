@@ -31,6 +31,8 @@ UNITS = [
     ("efta_attn_inst.cu", ["-DEFTA_INST_D=128"]),
     ("efta_attn_inst.cu", ["-DEFTA_INST_D=64", "-DEFTA_INST_INJ=1"]),
     ("efta_attn_inst.cu", ["-DEFTA_INST_D=128", "-DEFTA_INST_INJ=1"]),
+    ("efta_attn_inst.cu", ["-DEFTA_INST_D=64", "-DEFTA_INST_CAUSAL=1"]),
+    ("efta_attn_inst.cu", ["-DEFTA_INST_D=128", "-DEFTA_INST_CAUSAL=1"]),
     ("abft_gemm.cu", []),
     ("abft_verify.cu", []),
     ("efta_host.cu", []),
@@ -48,7 +50,7 @@ def _deps():
 
 
 def _obj(src, defs):
-    tag = "_".join(x.split("=")[-1] for x in defs) or "base"
+    tag = "_".join(x[2:].replace("EFTA_INST_", "").replace("=", "") for x in defs) or "base"
     return os.path.join(BUILD, f"{os.path.splitext(src)[0]}_{tag}.o")
 
 

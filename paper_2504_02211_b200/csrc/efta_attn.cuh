@@ -66,7 +66,24 @@ struct AttnParams {
     const __half* kc;          // [BH_kv*n, 32, D] checksum rows (workspace)
     int heads_q;               // query heads per batch entry (H)
     int kv_group;              // query heads per K/V head (GQA; 1 = multi-head attention)
+    int causal;                // causal build of the pair kernel was selected (key k visible to query q iff k <= q)
 };
+
+// Pair-kernel tile u -> (head, query pair, key blocks to visit). Causal: a query pair (2i, 2i+1)
+// needs key blocks 0..2i+1; a head's pairs are handed out longest first (head-major, so the
+// head's K / V stay in L2 while its tiles run).
+struct PairTile {
+    int head, pair, nblk;
+};
+template <bool CAUSAL>
+__device__ __forceinline__ PairTile pair_tile(const AttnParams& p, int u) {
+    const int npq = p.nblk / 2;
+    PairTile t;
+    t.head = u / npq;
+    t.pair = CAUSAL ? npq - 1 - u % npq : u % npq;
+    t.nblk = CAUSAL ? 2 * t.pair + 2 : p.nblk;
+    return t;
+}
 
 // Grouped-query attention: flat query head (b*H + h) -> flat K/V head (b*H_kv + h / group)
 __device__ __forceinline__ int kv_head(const AttnParams& p, int head) {

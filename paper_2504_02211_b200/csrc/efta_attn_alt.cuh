@@ -103,7 +103,7 @@ __device__ __noinline__ float pair_linear_residual(const AttnParams& p, const fl
     return lin;
 }
 
-template <int D, bool PROT, bool INJ>
+template <int D, bool PROT, bool INJ, bool CAUSAL>
 __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, float* ostage, uint64_t* s_full,
                                         uint64_t* s_free, uint64_t* p_ready, uint64_t* o_done, uint64_t* o_final,
                                         uint64_t* mx_early, uint64_t* mx_late, uint64_t* fin_bar, uint64_t* ack_bar,
@@ -155,12 +155,15 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
 
     // persistent: the (head, query-pair) tiles this cluster draws from the tile ring; every barrier phase runs on the
     // global block counter g = k*n + j (n is even, so block parity = warpgroup)
-    const int npq = n / 2;
     int it = 0;  // this warpgroup's block counter across tiles (= g >> 1)
+    int g_base = 0;                // global block counter at this tile's block 0
+    int ph_cnt[2] = {0, 0};        // blocks per warpgroup in the earlier tiles of each parity
     for (int k = 0;; ++k) {
     const int u = pair_next_tile(tinfo, t_full, t_empty, k, true);
     if (u < 0) break;
-    const int head = u / npq, qt = 2 * (u % npq) + static_cast<int>(rank);
+    const PairTile tt = pair_tile<CAUSAL>(p, u);
+    const int head = tt.head, qt = 2 * tt.pair + static_cast<int>(rank);
+    const int nt = tt.nblk;  // key blocks of this tile (causal: up to the pair's diagonal)
     // this tile's chain slots and barriers (tile parity); each barrier completes one phase per
     // block of its warpgroup in the tiles of this parity
     const int par = k & 1;
@@ -169,14 +172,15 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     uint64_t* my_late = mx_late + par * 8 + w * 4 + wq;
     uint64_t* pa_early = mx_early + par * 8 + (1 - w) * 4 + wq;
     uint64_t* pa_late = mx_late + par * 8 + (1 - w) * 4 + wq;
-    const int ph0 = (k >> 1) * npq;  // blocks per warpgroup in the earlier tiles of this parity
+    const int ph0 = ph_cnt[par];
+    ph_cnt[par] += nt / 2;
     const int seq_row0 = head * p.seq_len;
     if constexpr (INJ) tap.load(p, head, qt, row);
     // own sums, referenced to m_ref (the reference max of this warpgroup's last block);
     // INJ: l_w is the reference's full running denominator (lchain)
     float l_w = 0.0f, lb_w = 0.0f, m_ref = -CUDART_INF_F, m_true_last = -CUDART_INF_F;
-    for (int j = w; j < n; j += 2, ++it) {
-        const int g = k * n + j;
+    for (int j = w; j < nt; j += 2, ++it) {
+        const int g = g_base + j;
         if ((warp & 3) == 0) EFTA_TS(0, g);
         mbar_wait(&s_full[w], it & 1);
         if ((warp & 3) == 0) EFTA_TS(1, g);
@@ -192,6 +196,10 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         float m_true_prev = -CUDART_INF_F, m_run_prev = -CUDART_INF_F;
         float m_true, m_new, bm, psum_f = 0.0f;
         bool replaced_p = false;
+        // causal (fast build only): the diagonal block j == qt shows keys 0..row, a block past
+        // it (rank 0's last block of the pair) shows none; uniform per CTA
+        const bool masked = CAUSAL && !INJ && j >= qt;
+        const int mfrom = !masked ? kBlock : (j == qt ? row + 1 : 0);  // first masked key column
         for (int attempt = 0;; ++attempt) {
             uint32_t csr[16];
             // one x128 load where it pays (A/B: unprotected d=128 +4.7%, protected d=64 +2.8%);
@@ -212,6 +220,23 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             }
             int sc_fault_col = -1;
             float sc_fault_val = 0.0f;
+            if (masked) {
+                // causal: keys past the row's last visible one are masked (P = 0). The exp-stage
+                // check then covers each group's visible cells: the product of their P against
+                // exp(scale * c1_vis - n_vis * m), c1_vis = c1 minus the masked cells' scores
+                if (PROT) {
+#pragma unroll
+                    for (int x = 0; x < kStride; ++x) {
+                        float cm = 0.0f;
+#pragma unroll
+                        for (int l = 0; l < kBlock / kStride; ++l)
+                            if (x + kStride * l >= mfrom) cm = __fadd_rn(cm, pv[x + kStride * l]);
+                        csr[x] = __float_as_uint(__fsub_rn(__uint_as_float(csr[x]), cm));
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < kBlock; ++c) pv[c] = (c < mfrom) ? pv[c] : -CUDART_INF_F;
+            }
             if constexpr (INJ) {
                 // reference order: S = scale * (Q K^T) [GEMM1_OUT], row max + bias, running max [REDUCE_MAX]
                 tap.count = tap_snap;
@@ -279,8 +304,12 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             if (PROT) {
                 const float g16m = 16.0f * m_new;
 #pragma unroll
-                for (int x = 0; x < kStride; ++x)
-                    pc1v[x] = ex2_approx(__fsub_rn(__fmul_rn(__uint_as_float(csr[x]), scale), g16m) * kLog2e);
+                for (int x = 0; x < kStride; ++x) {
+                    // visible cells of group x: l < ceil((mfrom - x) / 8), at most 16
+                    const float gm = masked ? static_cast<float>(min(kBlock / kStride, max(0, (mfrom - x + kStride - 1) / kStride))) * m_new
+                                            : g16m;
+                    pc1v[x] = ex2_approx(__fsub_rn(__fmul_rn(__uint_as_float(csr[x]), scale), gm) * kLog2e);
+                }
             }
             float2 ps0 = make_float2(0.0f, 0.0f), ps1 = make_float2(0.0f, 0.0f);
             if constexpr (INJ) {
@@ -298,6 +327,31 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                     else ps0 = fadd2(ps0, e);
                     const int gg = (c & 7) >> 1;
                     prod_f[gg] = (c < kStride) ? e : fmul2(prod_f[gg], e);
+                }
+            } else if (masked) {
+                // the same exponentials; masked cells give P = 0 and stay out of the group products
+                const float mL = m_new * kLog2e;
+                const float2 sl2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-mL, -mL);
+#pragma unroll
+                for (int c = 0; c < kBlock; c += 2) {
+                    const float2 a = ffma2(make_float2(pv[c], pv[c + 1]), sl2, nm2);
+                    float2 e;
+                    if (exp_on_fma<D>(c)) {
+                        e = ex2_poly2(a);
+                    } else {
+                        e.x = ex2_approx(a.x);
+                        e.y = ex2_approx(a.y);
+                    }
+                    e.x = (c < mfrom) ? e.x : 0.0f;
+                    e.y = (c + 1 < mfrom) ? e.y : 0.0f;
+                    pk[c >> 1] = pack_half2(e.x, e.y);
+                    if ((c >> 1) & 1) ps1 = fadd2(ps1, e);
+                    else ps0 = fadd2(ps0, e);
+                    if (PROT) {
+                        const float2 ep = make_float2((c < mfrom) ? e.x : 1.0f, (c + 1 < mfrom) ? e.y : 1.0f);
+                        const int gg = (c & 7) >> 1;
+                        prod_f[gg] = (c < kStride) ? ep : fmul2(prod_f[gg], ep);
+                    }
                 }
             } else {
                 const float mL = m_new * kLog2e;
@@ -387,14 +441,16 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
                     tmem_ld32(s_addr + c4 * 32, r);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int x = 0; x < 32; ++x)
-                        p_loc[c4 * 32 + x] = ex2_col<D>(c4 * 32 + x, fmaf(__uint_as_float(r[x]), scale_log2, -mL));
+                    for (int x = 0; x < 32; ++x) {
+                        const int c = c4 * 32 + x;
+                        p_loc[c] = (c < mfrom) ? ex2_col<D>(c, fmaf(__uint_as_float(r[x]), scale_log2, -mL)) : 0.0f;
+                    }
                 }
             }
             int replaced = 0;
             exp_stage_slow<INJ, D, true>(p, s_addr, cs_addr, head, qt, j, row, exp_affected, exp_res, exp_viol,
                                          m_run_prev, m_new, bm, p_loc, replaced, tap, sc_fault_col, sc_fault_val,
-                                         rs, bo);
+                                         rs, bo, mfrom);
             if (replaced) {
                 if constexpr (INJ) {
 #pragma unroll
@@ -525,13 +581,14 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     // ------------------------------------------------ hand-over: warpgroup 0 -> 1
     // Warpgroup 1 ran the tile's last block (n is even): it merges the sums and runs the
     // epilogue while warpgroup 0 already starts the next tile.
+    const int g_last = g_base + nt - 1;
+    g_base += nt;
     if (w == 0) {
         xc->fin[row] = make_float4(INJ ? 0.0f : l_w, lb_w, m_ref, m_true_last);
         mbar_arrive(&fin_bar[par * 4 + wq]);
         if (INJ) flush_families(0.0f);
         continue;
     }
-    const int g_last = k * n + n - 1;
     if ((warp & 3) == 0) EFTA_TS(32, g_last);
     mbar_wait(&fin_bar[par * 4 + wq], static_cast<uint32_t>(k >> 1) & 1u);
     if ((warp & 3) == 0) EFTA_TS(33, g_last);

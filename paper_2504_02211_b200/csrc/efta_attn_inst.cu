@@ -1,6 +1,7 @@
 // efta_attn_inst.cu — instantiations of the fused attention kernels for one head dim
 // (EFTA_INST_D). EFTA_INST_INJ=1 builds only the fault-tap variant of the CTA-pair kernel
-// (its own translation unit so the variants compile in parallel); otherwise the unit holds
+// (its own translation unit so the variants compile in parallel), EFTA_INST_CAUSAL=1 only the
+// causal builds of the fast pair kernel; otherwise the unit holds
 // the single-CTA kernel (all modes x {fast, tap}), the fast pair kernels and the prepass.
 #include <algorithm>
 
@@ -14,6 +15,9 @@
 #ifndef EFTA_INST_INJ
 #define EFTA_INST_INJ 0
 #endif
+#ifndef EFTA_INST_CAUSAL
+#define EFTA_INST_CAUSAL 0
+#endif
 
 using namespace efta_sm100;
 
@@ -26,12 +30,12 @@ cudaError_t set_smem(K kern, uint32_t bytes) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
 }
 
-template <int D, int MODE, bool INJ>
+template <int D, int MODE, bool INJ, bool CAUSAL = false>
 cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const CUtensorMap& tkb,
                           const CUtensorMap& tkc, const CUtensorMap& tvt, const AttnParams& p, int bh,
                           cudaStream_t st) {
     using PL = PairLayout<D, MODE != 0>;
-    auto kern = efta_attn_pair_kernel<D, MODE, INJ>;
+    auto kern = efta_attn_pair_kernel<D, MODE, INJ, CAUSAL>;
     if (cudaError_t e = set_smem(kern, PL::SMEM_BYTES)) return e;
     int dev = 0, nsm = 0;
     if (cudaError_t e = cudaGetDevice(&dev)) return e;
@@ -43,7 +47,7 @@ cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const C
     return cudaGetLastError();
 }
 
-#if !EFTA_INST_INJ
+#if !EFTA_INST_INJ && !EFTA_INST_CAUSAL
 template <int D, int MODE, bool DBG>
 cudaError_t launch_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const CUtensorMap& tkc, const CUtensorMap& tvc, const AttnParams& p, int bh,
@@ -92,7 +96,15 @@ cudaError_t launch_encode_pair(bool prot, const void* k, const void* v, void* kc
 #define EFTA_CAT(a, b) EFTA_CAT2(a, b)
 #define EFTA_SFX EFTA_CAT(_d, EFTA_INST_D)
 
-#if EFTA_INST_INJ
+#if EFTA_INST_CAUSAL
+cudaError_t EFTA_CAT(efta_launch_attn_pair_causal, EFTA_SFX)(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
+                                                            const CUtensorMap& tkb, const CUtensorMap& tkc,
+                                                            const CUtensorMap& tvt, const AttnParams& p, int bh,
+                                                            cudaStream_t st) {
+    return mode == 0 ? launch_pair_t<EFTA_INST_D, 0, false, true>(tq, tka, tkb, tkc, tvt, p, bh, st)
+                     : launch_pair_t<EFTA_INST_D, 2, false, true>(tq, tka, tkb, tkc, tvt, p, bh, st);
+}
+#elif EFTA_INST_INJ
 cudaError_t EFTA_CAT(efta_launch_attn_pair_inj, EFTA_SFX)(const CUtensorMap& tq, const CUtensorMap& tka,
                                                          const CUtensorMap& tkb, const CUtensorMap& tkc,
                                                          const CUtensorMap& tvt, const AttnParams& p, int bh,

@@ -47,7 +47,9 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                                             float m_old, float& m_new, float& bm_hist,
                                             float* p_loc, int& replaced, ThreadTap& tap,
                                             int sc_fault_col, float sc_fault_val,
-                                            const RowScratch& rs, uint32_t bo = 0) {
+                                            const RowScratch& rs, uint32_t bo = 0, int mask_from = kBlock) {
+    // mask_from < kBlock (pair kernel, causal): key columns >= mask_from of this row are masked:
+    // P = 0 there, and the group checks run on the visible cells (c1 minus the masked scores)
     float sc[kBlock], raw[kBlock];
     float c1s[kStride], c2s[kStride];
     {
@@ -121,10 +123,22 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
         int changed = 0;
         bool still_bad = false;
         float rescan_res = 0.0f;
+        // visible part of each group (causal): the masked scores leave c1, n_vis cells remain
+        float c1v[kStride], nvis[kStride];
+        for (int x = 0; x < kStride; ++x) {
+            float cm = 0.0f;
+            int nv = 0;
+            for (int l = 0; l < kBlock / kStride; ++l) {
+                if (x + kStride * l >= mask_from) cm = __fadd_rn(cm, sc[x + kStride * l]);
+                else ++nv;
+            }
+            c1v[x] = mask_from < kBlock ? __fsub_rn(c1s[x], cm) : c1s[x];
+            nvis[x] = static_cast<float>(nv);
+        }
         if (affected) {
             const float before_m = m_new;
-            float bm = sc[0];
-            for (int c = 1; c < kBlock; ++c) bm = (bm < sc[c]) ? sc[c] : bm;  // row_max, no bias
+            float bm = mask_from > 0 ? sc[0] : -CUDART_INF_F;
+            for (int c = 1; c < mask_from; ++c) bm = (bm < sc[c]) ? sc[c] : bm;  // row_max, no bias
             float mm = (m_old < bm) ? bm : m_old;
             if (DBG) mm = tap(p, EFTA_REDUCE_MAX, j, 0, mm);
             m_new = mm;
@@ -144,14 +158,13 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
                             ? ex2_col<D>(c, fmaf(raw[c], scale_log2, -mL))
                             : ex2_approx(__fsub_rn(sc[c], mm) * kLog2e);
                 }
+                if (c >= mask_from) e = 0.0f;
                 if (__float_as_uint(e) != __float_as_uint(p_loc[c])) changed = 1;
                 p_loc[c] = e;
             }
-            const float g16m = 16.0f * mm;
-            const float g16m_old = 16.0f * before_m;
             for (int x = 0; x < kStride; ++x) {
-                const float pc_new = ex2_approx(__fsub_rn(c1s[x], g16m) * kLog2e);
-                const float pc_old = ex2_approx(__fsub_rn(c1s[x], g16m_old) * kLog2e);
+                const float pc_new = ex2_approx(__fsub_rn(c1v[x], nvis[x] * mm) * kLog2e);
+                const float pc_old = ex2_approx(__fsub_rn(c1v[x], nvis[x] * before_m) * kLog2e);
                 if (__float_as_uint(pc_new) != __float_as_uint(pc_old)) changed = 1;
             }
             replaced = 1;
@@ -159,8 +172,9 @@ __device__ __noinline__ void exp_stage_slow(const AttnParams& p, uint32_t s_addr
             still_bad = !isfinite(mm);
             for (int x = 0; x < kStride && !still_bad; ++x) {
                 float prod = 1.0f;
-                for (int l = 0; l < kBlock / kStride; ++l) prod = __fmul_rn(prod, p_loc[x + kStride * l]);
-                const float pc1 = ex2_approx(__fsub_rn(c1s[x], g16m) * kLog2e);
+                for (int l = 0; l < kBlock / kStride; ++l)
+                    if (x + kStride * l < mask_from) prod = __fmul_rn(prod, p_loc[x + kStride * l]);
+                const float pc1 = ex2_approx(__fsub_rn(c1v[x], nvis[x] * mm) * kLog2e);
                 if (!(prod > 0.0f && prod < CUDART_INF_F) || !(pc1 > 0.0f && pc1 < CUDART_INF_F)) {
                     still_bad = true;
                     rescan_res = CUDART_INF_F;

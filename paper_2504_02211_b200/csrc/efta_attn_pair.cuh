@@ -133,7 +133,7 @@ namespace efta_sm100 {
 // tm_kc: KC rows in 8-row boxes (protected), tm_vt: [V^T ; VC^T] rows of each block, box rows HN_V.
 // INJ: the fault-tap build (reference op sequence, eager rescale, taps at every FaultSite;
 // efta_attn_alt.cuh) — the `debug` variant of the same schedule.
-template <int D, int MODE, bool INJ>
+template <int D, int MODE, bool INJ, bool CAUSAL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_ka,
                       const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_kc,
@@ -216,10 +216,11 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             for (int k = 0;; ++k) {
                 const int u = pair_next_tile(tinfo, t_full, t_empty, k, false);
                 if (u < 0) break;
-                const int head = u / npq;
+                const PairTile tt = pair_tile<CAUSAL>(p, u);
+                const int head = tt.head;
                 const int kvh = kv_head(p, head);  // GQA: the K / checksum operands of the head's group
                 const int seq_row0 = kvh * p.seq_len;
-                for (int j = 0; j < n; ++j, ++g) {
+                for (int j = 0; j < tt.nblk; ++j, ++g) {
                     const int s = g % KS;
                     mbar_wait(&k_empty[s], ((g / KS) & 1) ^ 1);
                     uint8_t* dst = smem + L::OFF_K + s * L::K_STAGE;
@@ -277,7 +278,8 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                     u = pair_next_tile(tinfo, t_full, t_empty, k, false);
                     if (u < 0) break;
                 }
-                const int head = u / npq, qt = 2 * (u % npq) + static_cast<int>(rank);
+                const PairTile tt = pair_tile<CAUSAL>(p, u);
+                const int head = tt.head, qt = 2 * tt.pair + static_cast<int>(rank);
                 const int seq_row0 = head * p.seq_len;
                 // Q buffer k&1 was last read by the score MMAs of tile k-2
                 const int qb = k & 1;
@@ -288,7 +290,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                 for (int sub = 0; sub < NSUB; ++sub)
                     tma_load_2d_pair(smem + L::OFF_Q + qb * L::Q_BYTES + sub * 16384, &tm_q, qf, sub * 64,
                                      seq_row0 + qt * kBlock, kEvictFirst);
-                for (int j = 0; j < n; ++j, ++g) {
+                for (int j = 0; j < tt.nblk; ++j, ++g) {
                     const int s = g % VS;
                     mbar_wait(&v_empty[s], ((g / VS) & 1) ^ 1);
                     uint8_t* dst = smem + L::OFF_V + s * L::V_STAGE;
@@ -312,12 +314,14 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             const uint64_t dk0 = smem_desc_sw128(k_smem, 16, 1024);
             int g = 0;
             for (int k = 0;; ++k) {
-                if (pair_next_tile(tinfo, t_full, t_empty, k, true) < 0) break;
+                const int u = pair_next_tile(tinfo, t_full, t_empty, k, true);
+                if (u < 0) break;
+                const int nb = pair_tile<CAUSAL>(p, u).nblk;
                 const int qb = k & 1;
                 mbar_wait(qb ? q_full2 : q_full, (k >> 1) & 1);
                 tc_fence_after();
                 const uint64_t dqb = dq + ((qb * L::Q_BYTES) >> 4);
-                for (int j = 0; j < n; ++j, ++g) {
+                for (int j = 0; j < nb; ++j, ++g) {
                     if (g >= 2) {
                         mbar_wait(&s_free[g & 1], ((g - 2) >> 1) & 1);
                         EFTA_TS(7, g - 2);
@@ -336,7 +340,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                         }
                         commit2_both(&k_empty[s]);
                         commit2_both(&s_full[g & 1]);
-                        if (j == n - 1) commit2_both(&q_empty[qb]);
+                        if (j == nb - 1) commit2_both(&q_empty[qb]);
                     }
                     __syncwarp();
                     EFTA_TS(11, g - 2);
@@ -352,8 +356,10 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
             const uint32_t d_o = tmem + L::COL_O;
             int g = 0;
             for (int k = 0;; ++k) {
-                if (pair_next_tile(tinfo, t_full, t_empty, k, true) < 0) break;
-                for (int j = 0; j < n; ++j, ++g) {
+                const int u = pair_next_tile(tinfo, t_full, t_empty, k, true);
+                if (u < 0) break;
+                const int nb = pair_tile<CAUSAL>(p, u).nblk;
+                for (int j = 0; j < nb; ++j, ++g) {
                     EFTA_TS(10, g);
                     mbar_wait(&p_ready[g & 1], (g >> 1) & 1);
                     EFTA_TS(12, g);
@@ -373,7 +379,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
                         }
                         commit2_both(&v_empty[s]);
                         commit2_both(&o_done[g & 1]);
-                        if (j == n - 1) commit2_both(o_final);
+                        if (j == nb - 1) commit2_both(o_final);
                     }
                     __syncwarp();
                     EFTA_TS(13, g);
@@ -383,7 +389,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
         __syncwarp();
     } else {
         setmaxnreg_inc<232>();
-        row_alt<D, PROT, INJ>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH),
+        row_alt<D, PROT, INJ, CAUSAL>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH),
                               reinterpret_cast<float*>(smem + L::OFF_OSTG), s_full,
                               s_free, p_ready, o_done, o_final, mx_early, mx_late, fin_bar, ack_bar, o_free, tmem,
                               warp, lane, n, tinfo, t_full, t_empty, rank);

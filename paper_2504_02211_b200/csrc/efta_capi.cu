@@ -94,6 +94,12 @@ int validate(const efta_attn_desc* d) {
     if (bh > 65535) return fail(1, "efta_b200: batch*heads must be <= 65535");
     if (d->kv_heads < 0 || d->kv_heads > d->heads || (d->kv_heads > 0 && d->heads % d->kv_heads != 0))
         return fail(1, "efta_b200: kv_heads must divide heads (grouped-query attention)");
+    if (d->causal) {
+        if (d->mode != EFTA_MODE_NONE && d->mode != EFTA_MODE_EFTA_OPT)
+            return fail(1, "efta_b200: causal attention runs in modes NONE / EFTA_OPTIMIZED");
+        if (d->debug) return fail(1, "efta_b200: causal attention has no fault-tap build");
+        if ((d->seq_len / kBlock) % 2 != 0) return fail(1, "efta_b200: causal attention needs an even number of 128-row blocks");
+    }
     return 0;
 }
 
@@ -127,6 +133,7 @@ size_t ws_bytes(const efta_attn_desc* d) {
 // build of the same pair kernel. The single-CTA kernel serves mode EFTA (per-iteration output
 // check), odd tile counts, debug calls in mode NONE, and EFTA_NO_PAIR=1 A/B runs.
 bool use_pair(const efta_attn_desc* d) {
+    if (d->causal) return true;  // validated: even block count, NONE / EFTA_OPT, no taps
     if (d->mode == EFTA_MODE_EFTA || ((d->seq_len / kBlock) % 2) != 0) return false;
     if (d->debug && d->mode != EFTA_MODE_EFTA_OPT) return false;
     return std::getenv("EFTA_NO_PAIR") == nullptr;
@@ -314,6 +321,7 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     p.kc = reinterpret_cast<const __half*>(kc);
     p.heads_q = d->heads;
     p.kv_group = d->heads / kv_heads_of(d);
+    p.causal = d->causal;
     const bool dbg = d->debug != 0;
     cudaError_t e;
     if (pair)  // the persistent pair kernel's in-order tile counter (workspace scratch, int)
@@ -321,6 +329,9 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     if (pair && dbg)  // the tap build: maps as below
         e = (D == 64) ? efta_launch_attn_pair_inj_d64(tq, tk, tv, tkc, tvc, p, bh, st)
                       : efta_launch_attn_pair_inj_d128(tq, tk, tv, tkc, tvc, p, bh, st);
+    else if (pair && d->causal)
+        e = (D == 64) ? efta_launch_attn_pair_causal_d64(d->mode, tq, tk, tv, tkc, tvc, p, bh, st)
+                      : efta_launch_attn_pair_causal_d128(d->mode, tq, tk, tv, tkc, tvc, p, bh, st);
     else if (pair)  // maps: q, K half A, K half B (protected peer), KC, [V^T ; VC^T]
         e = (D == 64) ? efta_launch_attn_pair_d64(d->mode, tq, tk, tv, tkc, tvc, p, bh, st)
                       : efta_launch_attn_pair_d128(d->mode, tq, tk, tv, tkc, tvc, p, bh, st);

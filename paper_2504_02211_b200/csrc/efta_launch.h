@@ -27,6 +27,13 @@ cudaError_t efta_launch_attn_pair_d64(int mode, const CUtensorMap& tq, const CUt
 cudaError_t efta_launch_attn_pair_d128(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                        const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
                                        const efta_sm100::AttnParams& p, int bh, cudaStream_t st);
+// causal builds of the fast pair kernel (modes NONE / EFTA_OPT)
+cudaError_t efta_launch_attn_pair_causal_d64(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
+                                             const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
+                                             const efta_sm100::AttnParams& p, int bh, cudaStream_t st);
+cudaError_t efta_launch_attn_pair_causal_d128(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
+                                              const CUtensorMap& tkb, const CUtensorMap& tkc, const CUtensorMap& tvt,
+                                              const efta_sm100::AttnParams& p, int bh, cudaStream_t st);
 // fault-tap build of the pair kernel (EFTA_OPT; taps at every FaultSite, eager rescale)
 cudaError_t efta_launch_attn_pair_inj_d64(const CUtensorMap& tq, const CUtensorMap& tka, const CUtensorMap& tkb,
                                           const CUtensorMap& tkc, const CUtensorMap& tvt,
