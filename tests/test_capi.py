@@ -34,7 +34,7 @@ def _desc(**kw):
     from paper_2504_02211_b200 import _lib
     d = dict(batch=1, heads=12, seq_len=512, head_dim=64, block=128, stride=8, scale=0.0, mode=2,
              eps1=7e-6, eps2=0.48, eps_lin=0.48, observe_linear=0, rowmax_bias=0.0, debug=0,
-             checksums_ready=0, kv_heads=0)
+             checksums_ready=0, kv_heads=0, causal=0)
     d.update(kw)
     return _lib.AttnDesc(**d)
 
@@ -50,6 +50,10 @@ def _desc(**kw):
     (dict(mode=4), False, "unsupported mode"),
     (dict(kv_heads=4), True, ""),                              # grouped-query attention (F4)
     (dict(kv_heads=5), False, "kv_heads must divide heads"),
+    (dict(causal=1), True, ""),                                # causal pair kernel (F4)
+    (dict(causal=1, mode=1), False, "causal attention runs in modes"),
+    (dict(causal=1, debug=1), False, "causal attention has no fault-tap build"),
+    (dict(causal=1, seq_len=384), False, "causal attention needs an even number"),
 ])
 def test_validate_mirrors_attnconfig(kw, ok, msg):
     from paper_2504_02211_b200 import _lib
