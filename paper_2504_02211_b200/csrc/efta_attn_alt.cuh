@@ -644,7 +644,12 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     if (PROT) {
         // denominator range restriction (snvr.cpp:161-182, efta.cpp:289-310)
         const float upper = static_cast<float>(p.seq_len);
-        const bool bad = !isfinite(l_run) || l_run < lb || l_run > upper;
+        // the fast build forms P as ex2(fma(S, scale*log2e, -m*log2e)) (and partly on the FMA
+        // pipe), so the max cell's P can sit an ulp below the bound's exp(bm - m) = 1: a row whose
+        // sum is that single term (causal row 0) would be "restricted" by rounding alone. The
+        // comparison allows 2^-21 relative there; the tap build keeps the reference's exact test.
+        const float lb_cmp = INJ ? lb : __fmul_rn(lb, 1.0f - 0x1p-21f);
+        const bool bad = !isfinite(l_run) || l_run < lb_cmp || l_run > upper;
         double viol = 0.0;
         if (bad) {
             viol = !isfinite(l_run) ? CUDART_INF
