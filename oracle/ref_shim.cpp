@@ -14,6 +14,7 @@
 //   verify_locate_correct   include/efta/abft.hpp:58-60
 //   sample_random_plan      include/efta/fault.hpp:65-66
 //   Rng / trial_seed        include/efta/rng.hpp:19-58
+//   calibrate_thresholds / threshold_sweep   include/efta/campaign.hpp:87-110
 #include <cstring>
 #include <exception>
 #include <string>
@@ -21,6 +22,7 @@
 
 #include "efta/abft.hpp"
 #include "efta/attention.hpp"
+#include "efta/campaign.hpp"
 #include "efta/efta.hpp"
 #include "efta/fault.hpp"
 #include "efta/half.hpp"
@@ -244,6 +246,30 @@ int eref_verify_locate_correct(int rows, int cols, int stride, float* t, const f
             verify_locate_correct(mt, cp, eps, nullptr, row_eps_mult ? &mult : nullptr);
         to_ptr(mt, t);
         fill_report(r, rep);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// calibrate_thresholds + threshold_sweep (src/campaign.cpp:261-357): the base thresholds from
+// `cal_trials` clean observation runs (x safety), then `points` log-spaced multipliers
+int eref_threshold_sweep(int n, int d, int block, int stride, int mode, int cal_trials, double safety,
+                         uint64_t cal_seed, int trials, uint64_t seed, int points, double* base,
+                         double* mult, double* det, double* fa) {
+    try {
+        AttnConfig cfg(n, d, block, stride);
+        CalibrationResult cal = calibrate_thresholds(cfg, static_cast<FTMode>(mode), cal_trials, safety, cal_seed);
+        base[0] = cal.thr.eps1;
+        base[1] = cal.thr.eps2;
+        base[2] = cal.thr.eps_lin;
+        auto sw = threshold_sweep(cfg, static_cast<FTMode>(mode), cal.thr, trials, seed, points);
+        for (int i = 0; i < points; ++i) {
+            mult[i] = sw[i].multiplier;
+            det[i] = sw[i].detection_rate;
+            fa[i] = sw[i].false_alarm_rate;
+        }
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();
