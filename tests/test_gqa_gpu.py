@@ -98,3 +98,23 @@ def test_gqa_host_path_chunked_matches_device():
     assert np.array_equal(ho.view(np.uint32), o.cpu().numpy().view(np.uint32))
     assert np.array_equal(hm, m.cpu().numpy()) and np.array_equal(hl, l.cpu().numpy())
     assert cnt.detections == 0 and cnt.failed == 0
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_gqa_causal(d):
+    """Grouped-query and causal together (a decoder with GQA): each query head against its
+    group's K / V with the causal mask, vs float64."""
+    from paper_2504_02211_b200 import Thresholds, efta_forward
+    seq = 512
+    q, k, v = _inputs(900 + d, seq, d)
+    o, rep = efta_forward(_dev(q), _dev(k), _dev(v), mode="efta-opt", thr=Thresholds(1e-4, 1e-3, 1e-3), causal=True)
+    o = o.cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            qq, kk, vv = (x.astype(np.float64) for x in (q[b, h], k[b, _kv(h)], v[b, _kv(h)]))
+            s = qq @ kk.T / np.sqrt(d)
+            s[np.triu_indices(seq, 1)] = -np.inf
+            p = np.exp(s - s.max(axis=1, keepdims=True))
+            ref = (p @ vv) / p.sum(axis=1, keepdims=True)
+            assert rel_err(o[b, h], ref) <= TOL, (b, h)
+    assert rep.detections == 0 and not rep.failed
