@@ -28,7 +28,7 @@ def test_detector_curves_match_reference():
     g, ref = res["gpu"]["points"], res["reference"]["points"]
     assert len(g) == len(ref) == 10
     for (mg, dg, fg), (mr, dr, fr) in zip(g, ref):
-        assert abs(mg - mr) < 1e-9 * mr
+        assert abs(mg - mr) < 1e-5 * mr  # printed with 6 significant digits
         assert fg == fr, (mg, fg, fr)
         assert abs(dg - dr) <= 0.1, (mg, dg, dr)
     # monotone: looser thresholds never raise either rate (reference acceptance check 10)
