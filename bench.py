@@ -312,6 +312,26 @@ def suite(dev):
     cz["shape"] = {"batch": b, "heads": h, "seq_len": s_, "head_dim": d}
     out["causal"] = cz
     del q, k, v
+    # KV-cache decode (F4): one query row per head against C4-sized caches, the caches'
+    # checksum operands encoded once (steady-state decode); HBM-bound, bytes = K + V (+ KC, VC)
+    from paper_2504_02211_b200 import EftaDecode
+    b, h, s_, d = 32, 32, 8192, 128
+    qd = synth_inputs(51, (b, h, d), dev)
+    kd = synth_inputs(52, (b, h, s_, d), dev)
+    vd = synth_inputs(53, (b, h, s_, d), dev)
+    dz = {"shape": {"batch": b, "heads": h, "cache_len": s_, "head_dim": d}}
+    for mode in ("efta-opt", "none"):
+        op = EftaDecode(b, h, s_, d, mode=mode, thr=thr, device=dev)
+        op.encode(kd, vd)
+        ms = _time_cuda(lambda: op(qd, kd, vd, cache_encoded=True), iters=10)
+        kv = 2 * b * h * s_ * d * 2
+        cs = (b * h * (s_ // 128) * 32 * d * 2 + b * h * s_ * 64 * 2) if mode == "efta-opt" else 0
+        dz[f"decode_{mode}_ms"] = round(ms, 4)
+        dz[f"decode_{mode}_gbps"] = round((kv + cs) / (ms * 1e-3) / 1e9, 1)
+        dz[f"decode_{mode}_detections"] = op.report().detections
+        del op
+    out["decode"] = dz
+    del qd, kd, vd
     return out
 
 

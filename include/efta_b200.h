@@ -26,6 +26,7 @@
  *   efta_encode_strided_f32  encode_strided on a device tile, abft.hpp:38
  *   efta_verify_locate_correct_f32  verify_locate_correct on a device tile, abft.hpp:58-60
  *   efta_flip_bit            efta::flip_bit                 include/efta/fault.hpp:33
+ *   efta_decode_fwd_f16      (none: KV-cache decode, row 0 of efta_forward, a reference non-goal)
  */
 #ifndef EFTA_B200_H
 #define EFTA_B200_H
@@ -90,6 +91,17 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
                            const uint16_t* v, float* o, float* m_out, float* l_out,
                            const efta_fault_spec* faults, int n_faults, efta_event* events,
                            int ev_cap, efta_fired* fired, int fired_cap, efta_counters* counters);
+
+/* KV-cache decode (not a reference feature): one query row per head,
+ * q [batch*heads, head_dim], against the caches k, v [batch*kv_heads, seq_len, head_dim] (fp16
+ * bits); o [batch*heads, head_dim] fp32, m_out / l_out [batch*heads]. The reference algorithm
+ * for that row (it is row 0 of efta_forward(q, K, V)): eager online softmax over the 128-key
+ * blocks, EFTA-optimized checks (mode EFTA_OPTIMIZED) or none (NONE). HBM-bound, CUDA cores.
+ * workspace: efta_attn_workspace_bytes(d); checksums_ready = 1 skips re-encoding the cache's
+ * checksum operands (efta_attn_encode_kv_f16 into the workspace layout). */
+int efta_decode_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                        float* o, float* m_out, float* l_out, void* workspace, size_t workspace_bytes,
+                        efta_event* events, int ev_cap, efta_counters* counters, void* stream);
 
 /* Strided checksum operands of K and V only (the encode prepass the forward runs
  * internally); kc: [BH*nblk*32, head_dim] fp16, vc: [BH*nblk*128, 64] fp16. */

@@ -5,7 +5,8 @@ this package is the host-side mirror of the reference operator API. Attributes
 are resolved lazily so `python -m paper_2504_02211_b200.build` works before the
 library exists; any compute entry point raises if the library is missing.
 """
-_ATTN = ("EftaAttention", "FaultSpec", "FTReport", "Thresholds", "efta_forward", "validate_plan")
+_ATTN = ("EftaAttention", "FaultSpec", "FTReport", "Thresholds", "efta_forward", "validate_plan",
+         "EftaDecode", "efta_decode")
 _LIB = ("ConfigError", "EftaError", "SITES", "KINDS", "STATUS")
 _FFN = ("AbftLinear", "abft_gemm")
 _LAYER = ("FTTransformerLayer",)

@@ -75,6 +75,8 @@ def _load():
     lib.efta_attn_fwd_host_f16.argtypes = [C.POINTER(AttnDesc), vp, vp, vp, vp, vp, vp, vp,
                                            C.c_int, vp, C.c_int, vp, C.c_int, vp]
     lib.efta_attn_encode_kv_f16.argtypes = [C.POINTER(AttnDesc), vp, vp, vp, vp, vp]
+    lib.efta_decode_fwd_f16.argtypes = [C.POINTER(AttnDesc), vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp,
+                                        C.c_int, vp, vp]
     lib.efta_flip_bit.restype = C.c_float
     lib.efta_flip_bit.argtypes = [C.c_float, C.c_int, C.c_int]
     if hasattr(lib, "efta_abft_gemm_f16"):

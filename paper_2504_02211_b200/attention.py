@@ -250,3 +250,82 @@ def efta_forward(q, k, v, mode="efta-opt", thr: Thresholds | None = None, faults
     o, m, l = op(q4, k4, v4)
     rep = op.report(m.reshape(shape[:-1]), l.reshape(shape[:-1]))
     return o.reshape(shape), rep
+
+
+class EftaDecode:
+    """KV-cache decode (not a reference feature): one query row per head
+    against K / V caches [batch, kv_heads, seq_len, head_dim] — the reference algorithm for that
+    row (row 0 of efta_forward(q, K, V)) with EFTA-optimized checks, HBM-bound (csrc/decode.cu).
+    Owns the workspace holding the cache's checksum operands: `encode(k, v)` once, then decode
+    steps with `cache_encoded=True` skip re-encoding."""
+
+    def __init__(self, batch, heads, seq_len, head_dim, mode="efta-opt", thr=None, scale=0.0,
+                 kv_heads=None, ev_cap=1024, device="cuda"):
+        self.shape = (batch, heads, seq_len, head_dim)
+        self.kv_heads = heads if not kv_heads else int(kv_heads)
+        self.mode = mode
+        self.thr = thr or Thresholds()
+        self.desc = _desc(batch, heads, seq_len, head_dim, mode, self.thr, scale, False, 0.0, False, 128, 8,
+                          self.kv_heads)
+        check(lib.efta_attn_validate(C.byref(self.desc)))
+        dev = torch.device(device)
+        self.workspace = torch.empty(lib.efta_attn_workspace_bytes(C.byref(self.desc)), dtype=torch.uint8, device=dev)
+        self.counters = torch.zeros(C.sizeof(_lib.Counters), dtype=torch.uint8, device=dev)
+        self.ev_cap = ev_cap
+        self.events = torch.zeros(max(1, ev_cap) * C.sizeof(_lib.Event), dtype=torch.uint8, device=dev)
+
+    def encode(self, k, v, stream=None):
+        """Checksum operands of the caches into the workspace (efta_attn_encode_kv_f16)."""
+        st = stream if stream is not None else torch.cuda.current_stream(k.device)
+        ws = self.workspace.data_ptr()
+        b, h, s, d = self.shape
+        kc_bytes = ((b * self.kv_heads * (s // 128) * 32 * d * 2) + 255) // 256 * 256
+        check(lib.efta_attn_encode_kv_f16(C.byref(self.desc), k.data_ptr(), v.data_ptr(), ws, ws + kc_bytes,
+                                          st.cuda_stream))
+
+    def __call__(self, q, k, v, o=None, cache_encoded=False, stream=None):
+        b, h, s, d = self.shape
+        for t_, n_ in ((q, b * h * d), (k, b * self.kv_heads * s * d), (v, b * self.kv_heads * s * d)):
+            if t_.dtype != torch.float16 or not t_.is_cuda or not t_.is_contiguous() or t_.numel() != n_:
+                raise _lib.ConfigError("efta_decode: q [B,H,d] and k/v [B,H_kv,S,d] contiguous CUDA fp16")
+        if o is None:
+            o = torch.empty((b, h, d), dtype=torch.float32, device=q.device)
+        m = torch.empty((b, h), dtype=torch.float32, device=q.device)
+        l = torch.empty((b, h), dtype=torch.float32, device=q.device)
+        self.desc.checksums_ready = 1 if cache_encoded else 0
+        st = stream if stream is not None else torch.cuda.current_stream(q.device)
+        check(lib.efta_decode_fwd_f16(C.byref(self.desc), q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                      m.data_ptr(), l.data_ptr(), self.workspace.data_ptr(), self.workspace.numel(),
+                                      self.events.data_ptr(), self.ev_cap, self.counters.data_ptr(),
+                                      st.cuda_stream))
+        return o, m, l
+
+    def report(self) -> FTReport:
+        cnt = _lib.Counters.from_buffer_copy(bytes(self.counters.cpu().numpy()))
+        rep = FTReport(mode=self.mode, detections=cnt.detections, corrections=cnt.corrections,
+                       recomputes=cnt.recomputes, range_replacements=cnt.range_replacements,
+                       failed=bool(cnt.failed), family_max=tuple(cnt.family_max))
+        ne = min(cnt.n_events, self.ev_cap)
+        if ne:
+            raw = bytes(self.events[: ne * C.sizeof(_lib.Event)].cpu().numpy())
+            for i in range(ne):
+                e = _lib.Event.from_buffer_copy(raw, i * C.sizeof(_lib.Event))
+                rep.events.append(dict(kind=KINDS[e.kind], head=e.head, block_i=e.block_i, block_j=e.block_j,
+                                       status=STATUS[e.status], row=e.row, col=e.col, violations=e.violations,
+                                       corrections=e.corrections, checksum_repair=e.checksum_repair,
+                                       residual=e.residual, delta=e.delta))
+        return rep
+
+
+def efta_decode(q, k, v, mode="efta-opt", thr: Thresholds | None = None, scale=0.0):
+    """One decode step: q [B, H, d] (or [H, d]), k / v [B, H_kv, S, d] (or [H_kv, S, d]).
+    Returns (O fp32 [B, H, d], FTReport)."""
+    if q.dim() == 2:
+        q, k, v = q[None], k[None], v[None]
+    b, h, d = q.shape
+    _, hkv, s, _ = k.shape
+    op = EftaDecode(b, h, s, d, mode=mode, thr=thr, scale=scale, kv_heads=hkv, device=q.device)
+    o, m, l = op(q.contiguous(), k.contiguous(), v.contiguous())
+    rep = op.report()
+    rep.final_m, rep.final_l = m, l
+    return o, rep

@@ -37,6 +37,7 @@ UNITS = [
     ("abft_verify.cu", []),
     ("efta_host.cu", []),
     ("decoupled.cu", []),
+    ("decode.cu", []),
 ]
 
 

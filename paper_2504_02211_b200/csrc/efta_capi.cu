@@ -18,6 +18,12 @@
 #include "efta_launch.h"
 #include "efta_encode.cuh"
 
+namespace efta_decode {  // csrc/decode.cu
+size_t part_bytes(int bh, int nblk, int d, int nsm);
+cudaError_t launch(int d, bool prot, const efta_sm100::AttnParams& p, int bh, const void* q, const void* k,
+                   const void* v, const void* kc, const void* vc, float* part, int nsm, cudaStream_t st);
+}
+
 namespace efta_dec {  // csrc/decoupled.cu
 size_t workspace_bytes(int bh, int N, int D);
 std::string forward(const efta_sm100::AttnParams& base, int bh, int N, int D, const __half* q, const __half* k,
@@ -106,8 +112,14 @@ int validate(const efta_attn_desc* d) {
 // Workspace: [KC: bh*n*32*d fp16] [R2: max(single-CTA VC bh*n*128*64, pair V^T+VC^T
 // bh*n*(d+32)*128) fp16] [scratch: 256 B, the persistent pair kernel tile counter]. All offsets 256-byte aligned.
 struct WsLayout {
-    size_t kc, r2, scratch, total;
+    size_t kc, r2, scratch, part, total;
 };
+int device_sms() {
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        nsm = 148;
+    return nsm;
+}
 int kv_heads_of(const efta_attn_desc* d) { return d->kv_heads > 0 ? d->kv_heads : d->heads; }
 
 WsLayout ws_layout(const efta_attn_desc* d) {
@@ -119,7 +131,9 @@ WsLayout ws_layout(const efta_attn_desc* d) {
     w.r2 = al(bh * nblk * 32 * d->head_dim * sizeof(__half));
     const size_t r2 = std::max(bh * nblk * 128 * 64, bh * nblk * (d->head_dim + 32) * 128) * sizeof(__half);
     w.scratch = w.r2 + al(r2);
-    w.total = w.scratch + 256;  // scratch: the persistent pair kernel's tile counter
+    w.part = w.scratch + 256;  // scratch: the persistent pair kernel's tile counter
+    // decode: the split-KV partial results of every query row
+    w.total = w.part + al(efta_decode::part_bytes(d->batch * d->heads, static_cast<int>(nblk), d->head_dim, device_sms()));
     return w;
 }
 size_t ws_bytes(const efta_attn_desc* d) {
@@ -339,6 +353,52 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
         e = (D == 64) ? efta_launch_attn_d64(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st)
                       : efta_launch_attn_d128(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
     if (e != cudaSuccess) return fail(2, std::string("attention launch: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+int efta_decode_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                        float* o, float* m_out, float* l_out, void* workspace, size_t workspace_bytes,
+                        efta_event* events, int ev_cap, efta_counters* counters, void* stream) {
+    if (int rc = validate(d)) return rc;
+    if (d->mode != EFTA_MODE_NONE && d->mode != EFTA_MODE_EFTA_OPT)
+        return fail(1, "efta_decode_fwd_f16: modes NONE / EFTA_OPTIMIZED");
+    if (d->debug || d->causal) return fail(1, "efta_decode_fwd_f16: no fault-tap build; the query sees the whole cache");
+    if (!q || !k || !v || !o || !counters) return fail(1, "efta_decode_fwd_f16: null buffer");
+    const bool prot = d->mode == EFTA_MODE_EFTA_OPT;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(efta_counters), st));
+    const WsLayout wl = ws_layout(d);
+    char* wsb = static_cast<char*>(workspace);
+    void* kc = wsb ? wsb + wl.kc : nullptr;
+    void* vc = wsb ? wsb + wl.r2 : nullptr;
+    // the cache's strided checksum operands (KC, per-key VC); a decode loop that appends to the
+    // cache keeps them current and passes checksums_ready = 1
+    if (prot && !d->checksums_ready)
+        if (int rc = encode_kv(d, k, v, kc, vc, st)) return rc;
+    AttnParams p{};
+    p.seq_len = d->seq_len;
+    p.nblk = d->seq_len / kBlock;
+    p.n_heads_flat = d->batch * d->heads;
+    p.scale = d->scale == 0.0f ? 1.0f / std::sqrt(static_cast<float>(d->head_dim)) : d->scale;
+    p.scale_log2 = p.scale * kLog2e;
+    p.rowmax_bias = d->rowmax_bias;
+    p.eps1 = d->eps1;
+    p.eps2 = d->eps2;
+    p.eps_lin = d->eps_lin;
+    p.exp_lo = std::isfinite(d->eps1) ? static_cast<float>(std::exp(-d->eps1)) : 0.0f;
+    p.exp_hi = std::isfinite(d->eps1) ? static_cast<float>(std::exp(d->eps1)) : INFINITY;
+    p.o = o;
+    p.m_out = m_out;
+    p.l_out = l_out;
+    p.events = events;
+    p.ev_cap = events ? ev_cap : 0;
+    p.counters = counters;
+    p.heads_q = d->heads;
+    p.kv_group = d->heads / kv_heads_of(d);
+    if (workspace == nullptr || workspace_bytes < ws_bytes(d)) return fail(1, "efta_decode_fwd_f16: workspace too small");
+    cudaError_t e = efta_decode::launch(d->head_dim, prot, p, d->batch * d->heads, q, k, v, kc, vc,
+                                        reinterpret_cast<float*>(wsb + wl.part), device_sms(), st);
+    if (e != cudaSuccess) return fail(2, std::string("decode launch: ") + cudaGetErrorString(e));
     return 0;
 }
 
