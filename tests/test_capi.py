@@ -75,7 +75,10 @@ def test_workspace_size():
     al = lambda x: (x + 255) // 256 * 256  # noqa: E731
     kc = al(12 * 4 * 32 * 64 * 2)
     r2 = al(max(12 * 4 * 128 * 64, 12 * 4 * (64 + 32) * 128) * 2)
-    assert ws == kc + r2 + 256  # + the persistent kernel's tile counter
+    # + the persistent kernel's tile counter + the decode path's split-KV partials: 12 rows x
+    # splits x (m, l, lb, O[64], O.c[16]) fp32, splits = min(ceil(4 * SMs / 12), 4 / 2) = 2
+    part = al(12 * 2 * (3 + 64 + 16) * 4)
+    assert ws == kc + r2 + 256 + part
 
 
 def test_python_mirror_raises_config_error():
