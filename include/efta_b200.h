@@ -67,6 +67,12 @@ typedef struct {
                            Not a reference feature: modes NONE / EFTA_OPTIMIZED on the CTA-pair
                            kernel (even seq_len / 128), no fault-tap build. The diagonal block's
                            exp-stage check runs on each group's visible cells. */
+    int o_token_major;  /* 1: `o` receives fp16 [batch, seq_len, heads, head_dim] (token-major: the
+                           input of the output projection, no head-merge copy) instead of fp32
+                           [batch, heads, seq_len, head_dim]; the float* argument then points to
+                           that fp16 buffer. CTA-pair kernel configurations only (even seq_len /
+                           128, modes NONE / EFTA_OPTIMIZED), device entry point only. Not a
+                           reference feature (its attention returns fp32 per head). */
 } efta_attn_desc;
 
 const char* efta_last_error(void);
@@ -124,6 +130,12 @@ typedef struct {
     int n_tile;  /* 256 */
     double eps;  /* absolute threshold of verify_locate_correct (abft.hpp:58-60) */
     int debug;
+    /* Head-split output (0 = plain row-major [m, n]): with out_seq = S > 0, rows are tokens
+     * b*S + s and columns part*(H*dh) + h*dh + c (H = out_heads, dh = out_head_dim), and the
+     * element lands at y[part][b][h][s][c] — a fused QKV projection writes Q, K and V directly
+     * in the attention's [batch, heads, seq, head_dim] layout (parts = n / (H*dh)). Requires
+     * m % S == 0, n % (H*dh) == 0, dh % 8 == 0. Not a reference feature. */
+    int out_seq, out_heads, out_head_dim;
 } efta_gemm_desc;
 
 size_t efta_abft_weight_cs_bytes(const efta_gemm_desc* d);

@@ -26,7 +26,7 @@ class AttnDesc(C.Structure):
                 ("scale", C.c_float), ("mode", C.c_int), ("eps1", C.c_double),
                 ("eps2", C.c_double), ("eps_lin", C.c_double), ("observe_linear", C.c_int),
                 ("rowmax_bias", C.c_float), ("debug", C.c_int), ("checksums_ready", C.c_int),
-                ("kv_heads", C.c_int), ("causal", C.c_int)]
+                ("kv_heads", C.c_int), ("causal", C.c_int), ("o_token_major", C.c_int)]
 
 
 class FaultSpec(C.Structure):
@@ -52,7 +52,8 @@ class Counters(C.Structure):
 
 class GemmDesc(C.Structure):
     _fields_ = [("m", C.c_int), ("n", C.c_int), ("k", C.c_int), ("stride", C.c_int),
-                ("n_tile", C.c_int), ("eps", C.c_double), ("debug", C.c_int)]
+                ("n_tile", C.c_int), ("eps", C.c_double), ("debug", C.c_int),
+                ("out_seq", C.c_int), ("out_heads", C.c_int), ("out_head_dim", C.c_int)]
 
 
 class GemmFault(C.Structure):

@@ -144,14 +144,19 @@ class EftaAttention:
 
     def __init__(self, batch, heads, seq_len, head_dim, mode="efta-opt", thr=None, scale=0.0,
                  observe_linear=False, rowmax_bias=0.0, debug=False, block=128, stride=8,
-                 ev_cap=4096, fired_cap=256, device="cuda", kv_heads=None, causal=False):
+                 ev_cap=4096, fired_cap=256, device="cuda", kv_heads=None, causal=False,
+                 token_major_out=False):
         self.shape = (batch, heads, seq_len, head_dim)
+        # token_major_out: O comes back fp16 [batch, seq_len, heads, head_dim] (the output
+        # projection's input, written by the kernel's epilogue) instead of fp32 [b, h, s, d]
+        self.token_major_out = bool(token_major_out)
         # grouped-query attention: K / V carry kv_heads heads (query head h reads h // group)
         self.kv_heads = heads if not kv_heads else int(kv_heads)
         self.mode = mode
         self.thr = thr or Thresholds()
         self.desc = _desc(batch, heads, seq_len, head_dim, mode, self.thr, scale, observe_linear,
                           rowmax_bias, debug, block, stride, self.kv_heads, causal)
+        self.desc.o_token_major = 1 if token_major_out else 0
         check(lib.efta_attn_validate(C.byref(self.desc)))
         ws = lib.efta_attn_workspace_bytes(C.byref(self.desc))
         dev = torch.device(device)
@@ -183,7 +188,8 @@ class EftaAttention:
             if t.numel() != b * hh * s * d:
                 raise _lib.ConfigError("attention: Q/K/V must all be seq_len x head_dim")
         if o is None:
-            o = torch.empty((b, h, s, d), dtype=torch.float32, device=q.device)
+            o = (torch.empty((b, s, h, d), dtype=torch.float16, device=q.device) if self.token_major_out
+                 else torch.empty((b, h, s, d), dtype=torch.float32, device=q.device))
         if m is None:
             m = torch.empty((b, h, s), dtype=torch.float32, device=q.device)
         if l is None:

@@ -74,7 +74,18 @@ struct GemmParams {
     efta_event* events;
     int ev_cap;
     efta_counters* counters;
+    int sp_s, sp_h, sp_dh;  // head-split output layout (sp_s = 0: row-major [m, n])
 };
+
+// element index of output (row, col): row-major, or the head-split [part][b][h][s][c] layout
+__device__ __forceinline__ size_t y_index(const GemmParams& p, int row, int col) {
+    if (p.sp_s == 0) return static_cast<size_t>(row) * p.n + col;
+    const int hd = p.sp_h * p.sp_dh;
+    const int part = col / hd, rem = col - part * hd, h = rem / p.sp_dh, c = rem - h * p.sp_dh;
+    const int b = row / p.sp_s, s = row - b * p.sp_s;
+    return static_cast<size_t>(part) * p.m * hd +
+           ((static_cast<size_t>(b) * p.sp_h + h) * p.sp_s + s) * p.sp_dh + c;
+}
 
 struct RowScratchG {
     RowSlot* slots;
@@ -306,7 +317,15 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                     for (int i = 0; i < 8; ++i) {
                         const int r = 4 * i + (lane >> 3), q4 = lane & 7;
                         const uint4 w4 = *reinterpret_cast<const uint4*>(stg + r * 32 + ((q4 ^ (r & 7)) << 2));
-                        *reinterpret_cast<uint4*>(warp_base + static_cast<size_t>(r) * row_pitch + c * 128 + q4 * 16) = w4;
+                        uint8_t* dst;
+                        if (p.sp_s == 0) {
+                            dst = warp_base + static_cast<size_t>(r) * row_pitch + c * 128 + q4 * 16;
+                        } else {  // head split: the 16-byte piece stays inside one head row (dh % 8 == 0)
+                            constexpr int EPC = F32 ? 32 : 64;  // elements per 128-byte chunk
+                            dst = static_cast<uint8_t*>(p.y) +
+                                  y_index(p, grow - lane + r, nt * GN + half * 128 + c * EPC + q4 * (EPC / 8)) * (F32 ? 4 : 2);
+                        }
+                        *reinterpret_cast<uint4*>(dst) = w4;
                     }
                     __syncwarp();
                 }
@@ -393,8 +412,9 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                         verify_row<GN>(tloc, c1, c2, p.eps, rv);
                         for (int c = 0; c < GN; ++c)
                             if (__float_as_uint(tloc[c]) != __float_as_uint(before[c])) {
-                                if constexpr (F32) yrow32[c] = tloc[c];
-                                else yrow[c] = __float2half_rn(tloc[c]);
+                                const size_t yi = y_index(p, grow, nt * GN + c);
+                                if constexpr (F32) static_cast<float*>(p.y)[yi] = tloc[c];
+                                else static_cast<__half*>(p.y)[yi] = __float2half_rn(tloc[c]);
                             }
                     }
                 }
@@ -499,6 +519,15 @@ int gvalidate(const efta_gemm_desc* d) {
     if (d->m % GM) return gfail(1, "abft_gemm: m must be a multiple of 128");
     if (d->n % GN) return gfail(1, "abft_gemm: n must be a multiple of 256");
     if (d->k % GK) return gfail(1, "abft_gemm: k must be a multiple of 64");
+    if (d->out_seq < 0 || d->out_heads < 0 || d->out_head_dim < 0)
+        return gfail(1, "abft_gemm: head-split fields must be >= 0");
+    if (d->out_seq > 0) {
+        if (d->out_heads <= 0 || d->out_head_dim <= 0 || d->out_head_dim % 8 != 0)
+            return gfail(1, "abft_gemm: head split needs out_heads > 0 and out_head_dim a positive multiple of 8");
+        if (d->m % d->out_seq != 0) return gfail(1, "abft_gemm: head split: out_seq must divide m");
+        if (d->n % (d->out_heads * d->out_head_dim) != 0)
+            return gfail(1, "abft_gemm: head split: out_heads * out_head_dim must divide n");
+    }
     return 0;
 }
 
@@ -553,6 +582,11 @@ int efta_abft_gemm_ex(const efta_gemm_desc* d, const uint16_t* x, const uint16_t
     p.events = events;
     p.ev_cap = events ? ev_cap : 0;
     p.counters = counters;
+    if (d->out_seq > 0) {
+        p.sp_s = d->out_seq;
+        p.sp_h = d->out_heads;
+        p.sp_dh = d->out_head_dim;
+    }
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

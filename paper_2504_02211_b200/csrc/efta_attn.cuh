@@ -67,6 +67,7 @@ struct AttnParams {
     int heads_q;               // query heads per batch entry (H)
     int kv_group;              // query heads per K/V head (GQA; 1 = multi-head attention)
     int causal;                // causal build of the pair kernel was selected (key k visible to query q iff k <= q)
+    int o_tok;                 // 1: o holds fp16 [B, S, H, D] (token-major, the next linear layer's input)
 };
 
 // Pair-kernel tile u -> (head, query pair, key blocks to visit). Causal: a query pair (2i, 2i+1)

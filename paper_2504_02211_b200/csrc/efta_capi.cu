@@ -106,6 +106,15 @@ int validate(const efta_attn_desc* d) {
         if (d->debug) return fail(1, "efta_b200: causal attention has no fault-tap build");
         if ((d->seq_len / kBlock) % 2 != 0) return fail(1, "efta_b200: causal attention needs an even number of 128-row blocks");
     }
+    if (d->o_token_major != 0 && d->o_token_major != 1) return fail(1, "efta_b200: o_token_major must be 0 or 1");
+    if (d->o_token_major) {
+        if (d->mode != EFTA_MODE_NONE && d->mode != EFTA_MODE_EFTA_OPT)
+            return fail(1, "efta_b200: the token-major fp16 output runs in modes NONE / EFTA_OPTIMIZED");
+        if ((d->seq_len / kBlock) % 2 != 0)
+            return fail(1, "efta_b200: the token-major fp16 output needs an even number of 128-row blocks");
+        if (d->debug && d->mode != EFTA_MODE_EFTA_OPT)
+            return fail(1, "efta_b200: the token-major fp16 output's tap build is EFTA_OPTIMIZED");
+    }
     return 0;
 }
 
@@ -147,7 +156,7 @@ size_t ws_bytes(const efta_attn_desc* d) {
 // build of the same pair kernel. The single-CTA kernel serves mode EFTA (per-iteration output
 // check), odd tile counts, debug calls in mode NONE, and EFTA_NO_PAIR=1 A/B runs.
 bool use_pair(const efta_attn_desc* d) {
-    if (d->causal) return true;  // validated: even block count, NONE / EFTA_OPT, no taps
+    if (d->causal || d->o_token_major) return true;  // validated: even block count, NONE / EFTA_OPT, no taps
     if (d->mode == EFTA_MODE_EFTA || ((d->seq_len / kBlock) % 2) != 0) return false;
     if (d->debug && d->mode != EFTA_MODE_EFTA_OPT) return false;
     return std::getenv("EFTA_NO_PAIR") == nullptr;
@@ -336,6 +345,7 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     p.heads_q = d->heads;
     p.kv_group = d->heads / kv_heads_of(d);
     p.causal = d->causal;
+    p.o_tok = d->o_token_major;
     const bool dbg = d->debug != 0;
     cudaError_t e;
     if (pair)  // the persistent pair kernel's in-order tile counter (workspace scratch, int)
@@ -363,6 +373,7 @@ int efta_decode_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16
     if (d->mode != EFTA_MODE_NONE && d->mode != EFTA_MODE_EFTA_OPT)
         return fail(1, "efta_decode_fwd_f16: modes NONE / EFTA_OPTIMIZED");
     if (d->debug || d->causal) return fail(1, "efta_decode_fwd_f16: no fault-tap build; the query sees the whole cache");
+    if (d->o_token_major) return fail(1, "efta_decode_fwd_f16: fp32 [BH, rows, D] output only");
     if (!q || !k || !v || !o || !counters) return fail(1, "efta_decode_fwd_f16: null buffer");
     const bool prot = d->mode == EFTA_MODE_EFTA_OPT;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -407,6 +418,7 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
                            const efta_fault_spec* faults, int n_faults, efta_event* events,
                            int ev_cap, efta_fired* fired, int fired_cap, efta_counters* counters) {
     if (int rc = validate(d)) return rc;
+    if (d->o_token_major) return fail(1, "efta_attn_fwd_host_f16: fp32 [B, H, S, D] output only");
     // The (batch x head) units are independent (the reference's per-head loop,
     // src/campaign.cpp:175), so the host path streams them in chunks over three CUDA
     // streams: H2D of chunk i+1 and D2H of chunk i-1 overlap the kernels of chunk i

@@ -59,19 +59,30 @@ class AbftLinear:
         self.faults = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(self.weight.device)
 
     def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None, fp32_out: bool = False,
-                 checksums: torch.Tensor | None = None):
+                 checksums: torch.Tensor | None = None, head_split: tuple | None = None):
         """y = x @ weight.T (fp16, or fp32 with fp32_out). checksums, if given: a CUDA fp32
         tensor [tokens, out_features/256, 16] receiving each output tile's tensor-core
-        c1[8] | c2[8] per row (the reference's ChecksumPair per 256-wide tile)."""
+        c1[8] | c2[8] per row (the reference's ChecksumPair per 256-wide tile).
+        head_split = (seq, heads, head_dim): y comes back [parts, tokens/seq, heads, seq,
+        head_dim] (parts = out_features / (heads*head_dim)), written by the GEMM epilogue —
+        a fused QKV projection hands Q, K, V to the attention without a permute copy."""
         if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[1] != self.k:
             raise _lib.ConfigError("AbftLinear: x must be CUDA fp16 [tokens, in_features]")
         x = x.contiguous()
         m = x.shape[0]
+        split = (0, 0, 0)
+        shape = (m, self.n)
+        if head_split is not None:
+            seq, heads, hd = (int(v) for v in head_split)
+            split = (seq, heads, hd)
+            if seq <= 0 or heads <= 0 or hd <= 0 or m % seq or self.n % (heads * hd):
+                raise _lib.ConfigError("AbftLinear: head_split must tile [tokens, out_features]")
+            shape = (self.n // (heads * hd), m // seq, heads, seq, hd)
         if y is None:
-            y = torch.empty((m, self.n), dtype=torch.float32 if fp32_out else torch.float16, device=x.device)
+            y = torch.empty(shape, dtype=torch.float32 if fp32_out else torch.float16, device=x.device)
         if checksums is not None and (checksums.dtype != torch.float32 or checksums.numel() != m * (self.n // 256) * 16):
             raise _lib.ConfigError("AbftLinear: checksums must be fp32 [tokens, out/256, 16]")
-        desc = _lib.GemmDesc(m, self.n, self.k, 8, 256, self.eps, 1 if self.debug else 0)
+        desc = _lib.GemmDesc(m, self.n, self.k, 8, 256, self.eps, 1 if self.debug else 0, *split)
         check(lib.efta_abft_gemm_ex(
             C.byref(desc), x.data_ptr(), self.weight.data_ptr(), self.wcs.data_ptr(), y.data_ptr(),
             1 if y.dtype == torch.float32 else 0, checksums.data_ptr() if checksums is not None else None,

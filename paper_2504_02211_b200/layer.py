@@ -10,8 +10,9 @@ Structure (the paper applies strided ABFT to "all linear modules", PAPER.md:116,
     O   = EFTA(Q, K, V) (EftaAttention, EFTA-optimized)
     h   = X + O Wo^T    (AbftLinear)
     y   = h + GELU(h W1^T) W2^T   (AbftLinear x 2)
-The head split / merge and the GELU / residual adds are torch element-wise plumbing between
-the protected kernels (no normalisation layers: the reference protects only the GEMMs and
+The head split and merge are epilogue layouts of the protected kernels (the QKV GEMM writes
+[3, batch, heads, seq, head_dim], the attention writes fp16 token-major O); the GELU / residual
+adds are torch element-wise plumbing between them (no normalisation layers: the reference protects only the GEMMs and
 the attention). `protect=False` builds the unprotected twin of the same layer (cuBLAS
 linears, the same attention kernel in mode NONE) for the FT-overhead comparison.
 """
@@ -32,12 +33,13 @@ def _weight(n, k, gen, device):
 
 class FTTransformerLayer:
     def __init__(self, d_model=1280, n_heads=20, d_ff=5120, protect=True, thr=None, gemm_eps=1e-2,
-                 seed=0, device="cuda"):
+                 seed=0, device="cuda", fused_layout=True):
         if d_model % n_heads:
             raise ValueError("d_model must be a multiple of n_heads")
         self.d_model, self.n_heads, self.d_ff = d_model, n_heads, d_ff
         self.head_dim = d_model // n_heads
         self.protect = protect
+        self.fused_layout = fused_layout  # False: the head split / merge as torch copies (A/B)
         self.thr = thr or Thresholds(1e-4, 1e-3, 1e-3)
         gen = torch.Generator(device=device)
         gen.manual_seed(seed)
@@ -55,9 +57,11 @@ class FTTransformerLayer:
     def _attention(self, b, s):
         key = (b, s)
         if key not in self._attn:
+            # the fp16 token-major O output runs on the CTA-pair kernel (even seq / 128 blocks)
+            tok = self.fused_layout and (s // 128) % 2 == 0
             self._attn[key] = EftaAttention(b, self.n_heads, s, self.head_dim,
                                             mode="efta-opt" if self.protect else "none", thr=self.thr,
-                                            device=self.w["o"].device)
+                                            device=self.w["o"].device, token_major_out=tok)
         return self._attn[key]
 
     def flops(self, b, s):
@@ -69,11 +73,20 @@ class FTTransformerLayer:
         b, s, d = x.shape
         t = b * s
         x2 = x.reshape(t, d)
-        qkv = self._linear("qkv", x2)                                   # [t, 3d]
-        qkv = qkv.view(b, s, 3, self.n_heads, self.head_dim).permute(2, 0, 3, 1, 4).contiguous()
         attn = self._attention(b, s)
-        o, _, _ = attn(qkv[0], qkv[1], qkv[2])                          # [b, h, s, dh] fp32
-        o = o.to(torch.float16).permute(0, 2, 1, 3).reshape(t, d)
+        split = (s, self.n_heads, self.head_dim)
+        if self.protect and attn.token_major_out:
+            # the QKV GEMM's epilogue writes [3, b, h, s, dh] and the attention's epilogue fp16
+            # token-major O [b, s, h, dh] = the O projection's input: no head split / merge copies
+            qkv = self.lin["qkv"](x2, head_split=split)
+        else:
+            qkv = self._linear("qkv", x2)                               # [t, 3d] (cuBLAS twin)
+            qkv = qkv.view(b, s, 3, self.n_heads, self.head_dim).permute(2, 0, 3, 1, 4).contiguous()
+        o, _, _ = attn(qkv[0], qkv[1], qkv[2])
+        if attn.token_major_out:
+            o = o.view(t, d)                                            # fp16, already token-major
+        else:
+            o = o.to(torch.float16).permute(0, 2, 1, 3).reshape(t, d)  # [b, h, s, dh] fp32
         h = x2 + self._linear("o", o)
         f = self._linear("ff2", torch.nn.functional.gelu(self._linear("ff1", h)))
         return (h + f).view(b, s, d)

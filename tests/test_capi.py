@@ -34,7 +34,7 @@ def _desc(**kw):
     from paper_2504_02211_b200 import _lib
     d = dict(batch=1, heads=12, seq_len=512, head_dim=64, block=128, stride=8, scale=0.0, mode=2,
              eps1=7e-6, eps2=0.48, eps_lin=0.48, observe_linear=0, rowmax_bias=0.0, debug=0,
-             checksums_ready=0, kv_heads=0, causal=0)
+             checksums_ready=0, kv_heads=0, causal=0, o_token_major=0)
     d.update(kw)
     return _lib.AttnDesc(**d)
 
@@ -54,6 +54,13 @@ def _desc(**kw):
     (dict(causal=1, mode=1), False, "causal attention runs in modes"),
     (dict(causal=1, debug=1), False, "causal attention has no fault-tap build"),
     (dict(causal=1, seq_len=384), False, "causal attention needs an even number"),
+    (dict(o_token_major=1), True, ""),                         # fp16 token-major O (layer fusion)
+    (dict(o_token_major=1, causal=1, kv_heads=4, mode=0), True, ""),
+    (dict(o_token_major=1, mode=1), False, "token-major fp16 output runs in modes"),
+    (dict(o_token_major=1, mode=3), False, "token-major fp16 output runs in modes"),
+    (dict(o_token_major=1, seq_len=384), False, "token-major fp16 output needs an even number"),
+    (dict(o_token_major=1, mode=0, debug=1), False, "token-major fp16 output's tap build"),
+    (dict(o_token_major=2), False, "o_token_major must be 0 or 1"),
 ])
 def test_validate_mirrors_attnconfig(kw, ok, msg):
     from paper_2504_02211_b200 import _lib
@@ -164,3 +171,23 @@ def test_gqa_workspace_scales_with_kv_heads():
     mha = _lib.lib.efta_attn_workspace_bytes(C.byref(_desc(batch=2, heads=8, seq_len=1024)))
     gqa = _lib.lib.efta_attn_workspace_bytes(C.byref(_desc(batch=2, heads=8, seq_len=1024, kv_heads=2)))
     assert 0 < gqa < mha and mha / gqa > 3.5  # (the decode partials are per query head)
+
+
+@pytest.mark.parametrize("split,ok", [
+    ((0, 0, 0), True),
+    ((512, 10, 128), True),      # QKV of a 1280-wide model: [3, m/512, 10, 512, 128]
+    ((128, 7, 128), False),      # 896 does not divide n = 3840
+    ((100, 10, 128), False),     # seq must divide m
+    ((512, 10, 0), False),
+    ((512, 0, 128), False),
+    ((512, 20, 60), False),      # head_dim % 8
+    ((-1, 0, 0), False),
+])
+def test_gemm_head_split_validation(split, ok):
+    """efta_gemm_desc's head-split output fields (the fused QKV projection layout) are validated
+    host-side: efta_abft_weight_cs_bytes returns 0 for an invalid descriptor."""
+    from paper_2504_02211_b200 import _lib
+    d = _lib.GemmDesc(1024, 3840, 1280, 8, 256, 1e-2, 0, *split)
+    assert (_lib.lib.efta_abft_weight_cs_bytes(C.byref(d)) > 0) == ok
+    if not ok:
+        assert "head split" in _lib.last_error() or "head-split" in _lib.last_error()
