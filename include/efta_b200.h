@@ -155,6 +155,17 @@ int efta_abft_gemm_ex(const efta_gemm_desc* d, const uint16_t* x, const uint16_t
                       const efta_fault_spec* faults, int n_faults, efta_event* events, int ev_cap,
                       efta_counters* counters, void* stream);
 
+/* Same GEMM (fp16 output) with element-wise epilogues applied to each verified / corrected
+ * value before it is stored, the linear modules' neighbours in a transformer layer:
+ * y = act(half(X W^T)) (+ residual), activation EFTA_ACT_NONE or EFTA_ACT_GELU (erf form),
+ * residual NULL or fp16 [m, n] (row-major output only). The checksums protect the product
+ * (the reference's checksummed_gemm); the element-wise ops follow it. Not a reference API. */
+enum { EFTA_ACT_NONE = 0, EFTA_ACT_GELU = 1 };
+int efta_abft_gemm_fused_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w,
+                             const uint16_t* wcs, uint16_t* y, const uint16_t* residual,
+                             int activation, const efta_fault_spec* faults, int n_faults,
+                             efta_event* events, int ev_cap, efta_counters* counters, void* stream);
+
 /* ---- standalone strided ABFT on a device tile (reference abft.hpp:38-60) ----
  * encode_strided (src/abft.cpp:19-42): c1/c2 [rows, stride] of an fp32 tile [rows, cols].
  * verify_locate_correct (src/abft.cpp:65-187): repairs t in place, writes the report to device

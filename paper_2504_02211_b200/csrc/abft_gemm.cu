@@ -30,6 +30,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "../../include/efta_b200.h"
 #include "efta_attn.cuh"
@@ -75,7 +76,33 @@ struct GemmParams {
     int ev_cap;
     efta_counters* counters;
     int sp_s, sp_h, sp_dh;  // head-split output layout (sp_s = 0: row-major [m, n])
+    const __half* resid;    // fp16 output only: y = act(half(acc)) + resid (same layout as y), or null
+    int act;                // fp16 output only: EFTA_ACT_GELU applies erf-GELU to the verified value
 };
+
+// Epilogue element ops on the verified fp16 value (the torch restatement of the same layer rounds
+// the GEMM to fp16, then F.gelu / `+` compute in fp32 and round once more: identical bits).
+__device__ __forceinline__ float gelu_erf(float x) { return x * 0.5f * (1.0f + erff(x * 0.70710678118654752440f)); }
+__device__ __forceinline__ __half epi_one(__half h, const __half* r, int act) {
+    if (act == EFTA_ACT_GELU) h = __float2half_rn(gelu_erf(__half2float(h)));
+    if (r) h = __float2half_rn(__half2float(h) + __half2float(*r));
+    return h;
+}
+__device__ __forceinline__ uint4 epi_chunk(uint4 w4, const uint4* r4, int act) {
+    uint4 rv = r4 ? *r4 : make_uint4(0, 0, 0, 0);
+    uint32_t* w = &w4.x;
+    const uint32_t* rr = &rv.x;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+        const __half2 r2 = *reinterpret_cast<const __half2*>(&rr[i]);
+        const __half lo = epi_one(__low2half(h), r4 ? &r2.x : nullptr, act);
+        const __half hi = epi_one(__high2half(h), r4 ? &r2.y : nullptr, act);
+        h = __halves2half2(lo, hi);
+        w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    return w4;
+}
 
 // element index of output (row, col): row-major, or the head-split [part][b][h][s][c] layout
 __device__ __forceinline__ size_t y_index(const GemmParams& p, int row, int col) {
@@ -95,7 +122,8 @@ struct RowScratchG {
 
 // tm_w: W rows in boxes of 128 (single CTA) or 72 (pair); tm_wb: boxes of 56 (pair, the peer's
 // W rows next to its 16 checksum rows); tm_wc: checksum rows in boxes of 16.
-template <bool DBG, bool F32, bool PAIR>
+// EPI (fp16 output only): 0 plain store, 1 + residual, 2 GELU, 3 GELU + residual (p.act / p.resid)
+template <bool DBG, bool F32, bool PAIR, int EPI = 0>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                  const __grid_constant__ CUtensorMap tm_wb, const __grid_constant__ CUtensorMap tm_wc,
@@ -298,6 +326,14 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                 uint8_t* warp_base = rowbase - static_cast<size_t>(lane) * row_pitch;  // row 0 of the warp
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) {
+                    uint4 rr[(EPI & 1) ? 8 : 1];  // residual pieces of this chunk, loads in flight under the staging
+                    if constexpr ((EPI & 1) != 0) {
+                        const uint8_t* rbase = reinterpret_cast<const uint8_t*>(p.resid) + (warp_base - static_cast<uint8_t*>(p.y));
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            rr[i] = __ldcs(reinterpret_cast<const uint4*>(rbase + static_cast<size_t>(4 * i + (lane >> 3)) * row_pitch +
+                                                                       c * 128 + (lane & 7) * 16));
+                    }
 #pragma unroll
                     for (int q4 = 0; q4 < 8; ++q4) {
                         uint4 w4;
@@ -313,17 +349,31 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                         *reinterpret_cast<uint4*>(stg + lane * 32 + ((q4 ^ (lane & 7)) << 2)) = w4;
                     }
                     __syncwarp();
+                    constexpr int EPC = F32 ? 32 : 64;  // elements per 128-byte chunk
+                    size_t coloff = 0;  // head split: this lane's 16-byte piece's column part
+                    if (p.sp_s != 0) {
+                        const int col = nt * GN + half * 128 + c * EPC + (lane & 7) * (EPC / 8);
+                        const int hd = p.sp_h * p.sp_dh;
+                        const int part = col / hd, rem = col - part * hd, hh = rem / p.sp_dh;
+                        coloff = static_cast<size_t>(part) * p.m * hd + static_cast<size_t>(hh) * p.sp_s * p.sp_dh +
+                                 (rem - hh * p.sp_dh);
+                    }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int r = 4 * i + (lane >> 3), q4 = lane & 7;
-                        const uint4 w4 = *reinterpret_cast<const uint4*>(stg + r * 32 + ((q4 ^ (r & 7)) << 2));
+                        uint4 w4 = *reinterpret_cast<const uint4*>(stg + r * 32 + ((q4 ^ (r & 7)) << 2));
                         uint8_t* dst;
                         if (p.sp_s == 0) {
                             dst = warp_base + static_cast<size_t>(r) * row_pitch + c * 128 + q4 * 16;
                         } else {  // head split: the 16-byte piece stays inside one head row (dh % 8 == 0)
-                            constexpr int EPC = F32 ? 32 : 64;  // elements per 128-byte chunk
+                            const int row = grow - lane + r, b = row / p.sp_s;
                             dst = static_cast<uint8_t*>(p.y) +
-                                  y_index(p, grow - lane + r, nt * GN + half * 128 + c * EPC + q4 * (EPC / 8)) * (F32 ? 4 : 2);
+                                  (coloff + (static_cast<size_t>(b) * p.sp_h * p.sp_s + (row - b * p.sp_s)) * p.sp_dh) *
+                                      (F32 ? 4 : 2);
+                        }
+                        if constexpr (!F32) {
+                            if constexpr (EPI != 0)  // residual (prefetched) / activation
+                                w4 = epi_chunk(w4, (EPI & 1) ? &rr[i] : nullptr, (EPI & 2) ? EFTA_ACT_GELU : EFTA_ACT_NONE);
                         }
                         *reinterpret_cast<uint4*>(dst) = w4;
                     }
@@ -414,7 +464,10 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                             if (__float_as_uint(tloc[c]) != __float_as_uint(before[c])) {
                                 const size_t yi = y_index(p, grow, nt * GN + c);
                                 if constexpr (F32) static_cast<float*>(p.y)[yi] = tloc[c];
-                                else static_cast<__half*>(p.y)[yi] = __float2half_rn(tloc[c]);
+                                else
+                                    static_cast<__half*>(p.y)[yi] =
+                                        epi_one(__float2half_rn(tloc[c]), (EPI & 1) ? p.resid + yi : nullptr,
+                                                (EPI & 2) ? EFTA_ACT_GELU : EFTA_ACT_NONE);
                             }
                     }
                 }
@@ -550,10 +603,17 @@ int efta_abft_encode_weight_f16(const efta_gemm_desc* d, const uint16_t* w, uint
     return e == cudaSuccess ? 0 : gfail(2, cudaGetErrorString(e));
 }
 
-int efta_abft_gemm_ex(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w, const uint16_t* wcs, void* y,
-                      int y_f32, float* y_checksums, const efta_fault_spec* faults, int n_faults, efta_event* events,
-                      int ev_cap, efta_counters* counters, void* stream) {
+}  // extern "C"
+
+namespace {
+
+int gemm_run(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w, const uint16_t* wcs, void* y,
+             int y_f32, float* y_checksums, const uint16_t* resid, int act, const efta_fault_spec* faults,
+             int n_faults, efta_event* events, int ev_cap, efta_counters* counters, void* stream) {
     if (int rc = gvalidate(d)) return rc;
+    if (act != EFTA_ACT_NONE && act != EFTA_ACT_GELU) return gfail(1, "abft_gemm: unknown activation");
+    if ((resid || act) && y_f32) return gfail(1, "abft_gemm: residual / activation epilogues take the fp16 output");
+    if (resid && d->out_seq > 0) return gfail(1, "abft_gemm: the residual epilogue takes the row-major output");
     if (!x || !w || !wcs || !y || !counters) return gfail(1, "abft_gemm: null buffer");
     if (n_faults > 0 && !d->debug) return gfail(1, "abft_gemm: fault injection needs debug=1");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -582,6 +642,8 @@ int efta_abft_gemm_ex(const efta_gemm_desc* d, const uint16_t* x, const uint16_t
     p.events = events;
     p.ev_cap = events ? ev_cap : 0;
     p.counters = counters;
+    p.resid = reinterpret_cast<const __half*>(resid);
+    p.act = act;
     if (d->out_seq > 0) {
         p.sp_s = d->out_seq;
         p.sp_h = d->out_heads;
@@ -610,18 +672,42 @@ int efta_abft_gemm_ex(const efta_gemm_desc* d, const uint16_t* x, const uint16_t
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, kern, tx, tw, twb, twc, p);
     };
-    if (pair) {
-        if (y_f32)
-            e = d->debug ? launch(abft_gemm_kernel<true, true, true>, true) : launch(abft_gemm_kernel<false, true, true>, true);
-        else
-            e = d->debug ? launch(abft_gemm_kernel<true, false, true>, true) : launch(abft_gemm_kernel<false, false, true>, true);
-    } else {
-        if (y_f32)
-            e = d->debug ? launch(abft_gemm_kernel<true, true, false>, false) : launch(abft_gemm_kernel<false, true, false>, false);
-        else
-            e = d->debug ? launch(abft_gemm_kernel<true, false, false>, false) : launch(abft_gemm_kernel<false, false, false>, false);
-    }
+    const int epi = (resid ? 1 : 0) | (act == EFTA_ACT_GELU ? 2 : 0);
+    auto go = [&](auto dbg_c, auto pair_c) -> cudaError_t {
+        constexpr bool DB = decltype(dbg_c)::value, PR = decltype(pair_c)::value;
+        if (y_f32) return launch(abft_gemm_kernel<DB, true, PR>, PR);
+        switch (epi) {
+            case 1: return launch(abft_gemm_kernel<DB, false, PR, 1>, PR);
+            case 2: return launch(abft_gemm_kernel<DB, false, PR, 2>, PR);
+            case 3: return launch(abft_gemm_kernel<DB, false, PR, 3>, PR);
+            default: return launch(abft_gemm_kernel<DB, false, PR, 0>, PR);
+        }
+    };
+    using T = std::true_type;
+    using F = std::false_type;
+    if (pair)
+        e = d->debug ? go(T{}, T{}) : go(F{}, T{});
+    else
+        e = d->debug ? go(T{}, F{}) : go(F{}, F{});
     return e == cudaSuccess ? 0 : gfail(2, cudaGetErrorString(e));
+}
+
+}  // namespace
+
+extern "C" {
+
+int efta_abft_gemm_ex(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w, const uint16_t* wcs, void* y,
+                      int y_f32, float* y_checksums, const efta_fault_spec* faults, int n_faults, efta_event* events,
+                      int ev_cap, efta_counters* counters, void* stream) {
+    return gemm_run(d, x, w, wcs, y, y_f32, y_checksums, nullptr, EFTA_ACT_NONE, faults, n_faults, events, ev_cap,
+                    counters, stream);
+}
+
+int efta_abft_gemm_fused_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w, const uint16_t* wcs,
+                             uint16_t* y, const uint16_t* residual, int activation, const efta_fault_spec* faults,
+                             int n_faults, efta_event* events, int ev_cap, efta_counters* counters, void* stream) {
+    return gemm_run(d, x, w, wcs, y, 0, nullptr, residual, activation, faults, n_faults, events, ev_cap, counters,
+                    stream);
 }
 
 int efta_abft_gemm_f16(const efta_gemm_desc* d, const uint16_t* x, const uint16_t* w,

@@ -18,7 +18,7 @@ from . import _lib
 from ._lib import check, lib
 from .attention import FTReport, KINDS, STATUS
 
-_EXPORTS = ("efta_abft_gemm_f16", "efta_abft_gemm_ex", "efta_abft_encode_weight_f16", "efta_abft_weight_cs_bytes")
+_EXPORTS = ("efta_abft_gemm_f16", "efta_abft_gemm_ex", "efta_abft_gemm_fused_f16", "efta_abft_encode_weight_f16", "efta_abft_weight_cs_bytes")
 for _n in _EXPORTS:
     if not hasattr(lib, _n):
         raise ImportError(f"libefta_b200.so lacks {_n}: rebuild the library")
@@ -59,13 +59,17 @@ class AbftLinear:
         self.faults = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(self.weight.device)
 
     def __call__(self, x: torch.Tensor, y: torch.Tensor | None = None, fp32_out: bool = False,
-                 checksums: torch.Tensor | None = None, head_split: tuple | None = None):
+                 checksums: torch.Tensor | None = None, head_split: tuple | None = None,
+                 residual: torch.Tensor | None = None, activation: str | None = None):
         """y = x @ weight.T (fp16, or fp32 with fp32_out). checksums, if given: a CUDA fp32
         tensor [tokens, out_features/256, 16] receiving each output tile's tensor-core
         c1[8] | c2[8] per row (the reference's ChecksumPair per 256-wide tile).
         head_split = (seq, heads, head_dim): y comes back [parts, tokens/seq, heads, seq,
         head_dim] (parts = out_features / (heads*head_dim)), written by the GEMM epilogue —
-        a fused QKV projection hands Q, K, V to the attention without a permute copy."""
+        a fused QKV projection hands Q, K, V to the attention without a permute copy.
+        residual (fp16 [tokens, out_features]) / activation ("gelu"): element-wise epilogues on
+        the verified fp16 value, y = gelu(half(x @ W.T)) (+ residual) — the residual adds and
+        the FFN activation of a transformer layer without extra passes over HBM."""
         if x.dtype != torch.float16 or not x.is_cuda or x.dim() != 2 or x.shape[1] != self.k:
             raise _lib.ConfigError("AbftLinear: x must be CUDA fp16 [tokens, in_features]")
         x = x.contiguous()
@@ -83,6 +87,22 @@ class AbftLinear:
         if checksums is not None and (checksums.dtype != torch.float32 or checksums.numel() != m * (self.n // 256) * 16):
             raise _lib.ConfigError("AbftLinear: checksums must be fp32 [tokens, out/256, 16]")
         desc = _lib.GemmDesc(m, self.n, self.k, 8, 256, self.eps, 1 if self.debug else 0, *split)
+        faults = self.faults.data_ptr() if self.faults is not None else None
+        st = torch.cuda.current_stream(x.device).cuda_stream
+        if residual is not None or activation is not None:
+            if activation not in (None, "gelu"):
+                raise _lib.ConfigError("AbftLinear: activation must be None or 'gelu'")
+            if residual is not None and (residual.dtype != torch.float16 or not residual.is_cuda
+                                         or residual.shape != (m, self.n)):
+                raise _lib.ConfigError("AbftLinear: residual must be CUDA fp16 [tokens, out_features]")
+            if checksums is not None:
+                raise _lib.ConfigError("AbftLinear: the fused epilogues return no tile checksums")
+            res = residual.contiguous() if residual is not None else None
+            check(lib.efta_abft_gemm_fused_f16(
+                C.byref(desc), x.data_ptr(), self.weight.data_ptr(), self.wcs.data_ptr(), y.data_ptr(),
+                res.data_ptr() if res is not None else None, 1 if activation == "gelu" else 0,
+                faults, self.n_faults, self.events.data_ptr(), self.ev_cap, self.counters.data_ptr(), st))
+            return y
         check(lib.efta_abft_gemm_ex(
             C.byref(desc), x.data_ptr(), self.weight.data_ptr(), self.wcs.data_ptr(), y.data_ptr(),
             1 if y.dtype == torch.float32 else 0, checksums.data_ptr() if checksums is not None else None,

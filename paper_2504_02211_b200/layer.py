@@ -11,10 +11,13 @@ Structure (the paper applies strided ABFT to "all linear modules", PAPER.md:116,
     h   = X + O Wo^T    (AbftLinear)
     y   = h + GELU(h W1^T) W2^T   (AbftLinear x 2)
 The head split and merge are epilogue layouts of the protected kernels (the QKV GEMM writes
-[3, batch, heads, seq, head_dim], the attention writes fp16 token-major O); the GELU / residual
-adds are torch element-wise plumbing between them (no normalisation layers: the reference protects only the GEMMs and
-the attention). `protect=False` builds the unprotected twin of the same layer (cuBLAS
-linears, the same attention kernel in mode NONE) for the FT-overhead comparison.
+[3, batch, heads, seq, head_dim], the attention writes fp16 token-major O) and the residual adds
+and GELU are epilogue ops of the protected GEMMs, applied to the verified values
+(fused_layout=False: the same layer with torch copies and element-wise ops, bit-identical).
+No normalisation layers: the reference protects only the GEMMs and the attention.
+`protect=False` builds the unprotected twin of the same layer (cuBLAS linears with the residual
+adds as beta = 1 epilogues, torch GELU, the same attention kernel in mode NONE with the fp16
+token-major output, a torch head-split copy) for the FT-overhead comparison.
 """
 from __future__ import annotations
 
@@ -33,13 +36,14 @@ def _weight(n, k, gen, device):
 
 class FTTransformerLayer:
     def __init__(self, d_model=1280, n_heads=20, d_ff=5120, protect=True, thr=None, gemm_eps=1e-2,
-                 seed=0, device="cuda", fused_layout=True):
+                 seed=0, device="cuda", fused_layout=True, fused_gelu=False):
         if d_model % n_heads:
             raise ValueError("d_model must be a multiple of n_heads")
         self.d_model, self.n_heads, self.d_ff = d_model, n_heads, d_ff
         self.head_dim = d_model // n_heads
         self.protect = protect
         self.fused_layout = fused_layout  # False: the head split / merge as torch copies (A/B)
+        self.fused_gelu = fused_gelu      # True: GELU in the ff1 epilogue (measured slower: erff in the epilogue warps)
         self.thr = thr or Thresholds(1e-4, 1e-3, 1e-3)
         gen = torch.Generator(device=device)
         gen.manual_seed(seed)
@@ -87,6 +91,17 @@ class FTTransformerLayer:
             o = o.view(t, d)                                            # fp16, already token-major
         else:
             o = o.to(torch.float16).permute(0, 2, 1, 3).reshape(t, d)  # [b, h, s, dh] fp32
+        if self.fused_layout and self.protect:
+            # residual adds and GELU in the protected GEMMs' epilogues (after verification)
+            h = self.lin["o"](o, residual=x2)
+            f1 = (self.lin["ff1"](h, activation="gelu") if self.fused_gelu
+                  else torch.nn.functional.gelu(self.lin["ff1"](h)))
+            return self.lin["ff2"](f1, residual=h).view(b, s, d)
+        if self.fused_layout:
+            # unprotected twin: the residual adds as cuBLAS beta = 1 epilogues
+            h = torch.addmm(x2, o, self.w["o"].t())
+            f1 = torch.nn.functional.gelu(h @ self.w["ff1"].t())
+            return torch.addmm(h, f1, self.w["ff2"].t()).view(b, s, d)
         h = x2 + self._linear("o", o)
         f = self._linear("ff2", torch.nn.functional.gelu(self._linear("ff1", h)))
         return (h + f).view(b, s, d)

@@ -16,8 +16,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--iters", type=int, default=5)
 a = ap.parse_args()
 thr = Thresholds(1e-4, 1e-3, 1e-3)
-layers = {(p, f): FTTransformerLayer(1280, 20, 5120, protect=p, thr=thr, seed=1, fused_layout=f)
-          for p in (True, False) for f in (True, False)}
+layers = {(p, f): FTTransformerLayer(1280, 20, 5120, protect=p, thr=thr, seed=1, fused_layout=f != "copies",
+                                     fused_gelu=f == "fused")
+          for p in (True, False) for f in ("fused", "fused-nogelu", "copies")}
 
 
 def med_ms(fn):
@@ -39,9 +40,9 @@ g.manual_seed(3)
 for seq in (512, 2048, 8192, 16384):
     b = 16384 // seq
     x = torch.empty((b, seq, 1280), device="cuda").uniform_(-1, 1, generator=g).half()
-    fl = layers[(True, True)].flops(b, seq)
+    fl = layers[(True, "fused")].flops(b, seq)
     row = []
     for (p, f), lay in layers.items():
         ms = med_ms(lambda: lay(x))
-        row.append(f"{'prot' if p else 'unprot'}/{'fused' if f else 'copies'} {ms:.3f} ms {fl / ms / 1e9:.1f} TF/s")
+        row.append(f"{'prot' if p else 'unprot'}/{f} {ms:.3f} ms {fl / ms / 1e9:.1f} TF/s")
     print(f"S={seq} B={b}: " + " | ".join(row), flush=True)
