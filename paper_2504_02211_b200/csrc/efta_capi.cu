@@ -430,8 +430,12 @@ int efta_attn_fwd_host_f16(const efta_attn_desc* d, const uint16_t* q, const uin
     const bool gqa = kv_heads_of(d) != d->heads;
     const int units = gqa ? d->batch : bh;
     const int qh_unit = gqa ? d->heads : 1, kvh_unit = gqa ? kv_heads_of(d) : 1;
-    const int nchunk = (n_faults > 0 || fired) ? 1 : std::min(units, 32);  // small first-H2D / last-D2H tails
-    const int per = (units + nchunk - 1) / nchunk;
+    int max_chunks = 32;  // small first-H2D / last-D2H tails; EFTA_HOST_CHUNKS overrides (A/B)
+    if (const char* ev = std::getenv("EFTA_HOST_CHUNKS")) max_chunks = std::max(1, std::min(64, std::atoi(ev)));
+    const int want = (n_faults > 0 || fired) ? 1 : std::min(units, max_chunks);
+    const int per = (units + want - 1) / want;
+    // chunks actually used (e.g. 33 units in chunks of 2 -> 17): every chunk's counters are read back
+    const int nchunk = (units + per - 1) / per;
     struct Scratch {
         void* p = nullptr;
         size_t n = 0;

@@ -22,8 +22,10 @@ def _dev(x):
     return torch.from_numpy(x).to(torch.float16).cuda().contiguous()
 
 
-@pytest.mark.parametrize("d,seq,heads", [(64, 512, 16), (128, 512, 6)])
+@pytest.mark.parametrize("d,seq,heads", [(64, 512, 16), (128, 512, 6), (64, 256, 33)])
 def test_host_path_chunked_matches_device(d, seq, heads):
+    """(33 heads: chunks of 2 heads, 17 chunks used of the 32 allowed — every chunk's counters
+    are merged, none read back uninitialised)"""
     import torch
     from paper_2504_02211_b200 import EftaAttention, Thresholds, _lib
     q, k, v, _ = head_inputs(4242 + d, heads, seq, d)
