@@ -166,6 +166,11 @@ int efta_abft_gemm_fused_f16(const efta_gemm_desc* d, const uint16_t* x, const u
                              int activation, const efta_fault_spec* faults, int n_faults,
                              efta_event* events, int ev_cap, efta_counters* counters, void* stream);
 
+/* Element-wise erf GELU of an fp16 device tensor (n elements, 16-byte aligned; y may equal x):
+ * the FFN activation between the protected GEMMs of the FT-Transformer layer, bit-identical to
+ * torch.nn.functional.gelu. Not a reference API. */
+int efta_gelu_f16(const uint16_t* x, uint16_t* y, size_t n, void* stream);
+
 /* ---- standalone strided ABFT on a device tile (reference abft.hpp:38-60) ----
  * encode_strided (src/abft.cpp:19-42): c1/c2 [rows, stride] of an fp32 tile [rows, cols].
  * verify_locate_correct (src/abft.cpp:65-187): repairs t in place, writes the report to device

@@ -88,6 +88,7 @@ def _load():
         lib.efta_abft_weight_cs_bytes.argtypes = [C.POINTER(GemmDesc)]
         lib.efta_abft_gemm_ex.argtypes = [C.POINTER(GemmDesc), vp, vp, vp, vp, C.c_int, vp, vp, C.c_int,
                                           vp, C.c_int, vp, vp]
+        lib.efta_gelu_f16.argtypes = [vp, vp, C.c_size_t, vp]
         lib.efta_abft_gemm_fused_f16.argtypes = [C.POINTER(GemmDesc), vp, vp, vp, vp, vp, C.c_int, vp,
                                                  C.c_int, vp, C.c_int, vp, vp]
     return lib
@@ -100,7 +101,7 @@ EXPORTS = ["efta_last_error", "efta_attn_validate", "efta_attn_workspace_bytes",
            "efta_attn_fwd_f16", "efta_attn_fwd_host_f16", "efta_attn_encode_kv_f16",
            "efta_flip_bit", "efta_abft_gemm_f16", "efta_abft_encode_weight_f16",
            "efta_abft_weight_cs_bytes", "efta_trial_seed", "efta_gen_trial_f16",
-           "efta_classify_trial", "efta_abft_gemm_ex", "efta_abft_gemm_fused_f16", "efta_encode_strided_f32",
+           "efta_classify_trial", "efta_abft_gemm_ex", "efta_abft_gemm_fused_f16", "efta_gelu_f16", "efta_encode_strided_f32",
            "efta_verify_workspace_bytes", "efta_verify_locate_correct_f32"]
 
 

@@ -38,6 +38,7 @@ UNITS = [
     ("efta_host.cu", []),
     ("decoupled.cu", []),
     ("decode.cu", []),
+    ("elementwise.cu", []),
 ]
 
 

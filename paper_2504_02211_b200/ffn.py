@@ -128,6 +128,14 @@ class AbftLinear:
         return rep
 
 
+def gelu_(x: torch.Tensor) -> torch.Tensor:
+    """In-place erf GELU of a CUDA fp16 tensor (csrc/elementwise.cu; bit-identical to F.gelu)."""
+    if x.dtype != torch.float16 or not x.is_cuda or not x.is_contiguous():
+        raise _lib.ConfigError("gelu_: x must be a contiguous CUDA fp16 tensor")
+    check(lib.efta_gelu_f16(x.data_ptr(), x.data_ptr(), x.numel(), torch.cuda.current_stream(x.device).cuda_stream))
+    return x
+
+
 def _validate(desc) -> int:
     # efta_abft_weight_cs_bytes returns 0 on an invalid descriptor and sets the error
     return 0 if lib.efta_abft_weight_cs_bytes(C.byref(desc)) else 1

@@ -15,9 +15,11 @@ The head split and merge are epilogue layouts of the protected kernels (the QKV 
 and GELU are epilogue ops of the protected GEMMs, applied to the verified values
 (fused_layout=False: the same layer with torch copies and element-wise ops, bit-identical).
 No normalisation layers: the reference protects only the GEMMs and the attention.
-`protect=False` builds the unprotected twin of the same layer (cuBLAS linears with the residual
-adds as beta = 1 epilogues, torch GELU, the same attention kernel in mode NONE with the fp16
-token-major output, a torch head-split copy) for the FT-overhead comparison.
+The GELU is csrc/elementwise.cu's HBM-bound pass (bit-identical to F.gelu; in the ff1 epilogue
+it measured slower, fused_gelu=True). `protect=False` builds the unprotected twin of the same
+layer (cuBLAS linears with the residual adds as beta = 1 epilogues, the same GELU pass, the same
+attention kernel in mode NONE with the fp16 token-major output, a torch head-split copy) for the
+FT-overhead comparison.
 """
 from __future__ import annotations
 
@@ -26,7 +28,7 @@ import math
 import torch
 
 from .attention import EftaAttention, FTReport, Thresholds
-from .ffn import AbftLinear
+from .ffn import AbftLinear, gelu_
 
 
 def _weight(n, k, gen, device):
@@ -94,13 +96,12 @@ class FTTransformerLayer:
         if self.fused_layout and self.protect:
             # residual adds and GELU in the protected GEMMs' epilogues (after verification)
             h = self.lin["o"](o, residual=x2)
-            f1 = (self.lin["ff1"](h, activation="gelu") if self.fused_gelu
-                  else torch.nn.functional.gelu(self.lin["ff1"](h)))
+            f1 = self.lin["ff1"](h, activation="gelu") if self.fused_gelu else gelu_(self.lin["ff1"](h))
             return self.lin["ff2"](f1, residual=h).view(b, s, d)
         if self.fused_layout:
             # unprotected twin: the residual adds as cuBLAS beta = 1 epilogues
             h = torch.addmm(x2, o, self.w["o"].t())
-            f1 = torch.nn.functional.gelu(h @ self.w["ff1"].t())
+            f1 = gelu_(h @ self.w["ff1"].t())
             return torch.addmm(h, f1, self.w["ff2"].t()).view(b, s, d)
         h = x2 + self._linear("o", o)
         f = self._linear("ff2", torch.nn.functional.gelu(self._linear("ff1", h)))

@@ -209,3 +209,22 @@ def test_layer_fused_layouts_bit_identical(protect, s):
     assert a.report().detections == 0
     assert a._attn[(2, s)].token_major_out == (s == 512)
     np.testing.assert_equal(ya.shape, (2, s, 1280))
+
+
+@pytest.mark.parametrize("n", [16384 * 5120, 1000003, 7])
+def test_gelu_pass_bit_identical_to_torch(n):
+    """csrc/elementwise.cu's GELU (the layer's FFN activation) equals F.gelu on fp16 bit for bit,
+    including the ragged tail, infinities, huge / tiny magnitudes and subnormals (NaN as NaN)."""
+    import torch
+    from paper_2504_02211_b200.ffn import gelu_
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n)
+    x = (torch.randn(n, device="cuda", generator=g) * 4).half()
+    special = torch.tensor([float("inf"), float("-inf"), float("nan"), 65504.0, -65504.0, 6e-8, -6e-8,
+                            1e-5, -1e-5, 0.0, -0.0, -9.5, 9.5], device="cuda").half()
+    x[: min(n, special.numel())] = special[: min(n, special.numel())]
+    ref = torch.nn.functional.gelu(x)
+    y = gelu_(x.clone())
+    nan = torch.isnan(ref)
+    assert torch.equal(torch.isnan(y), nan)
+    assert torch.equal(_bits(y)[~nan], _bits(ref)[~nan])
