@@ -104,7 +104,8 @@ __device__ __noinline__ float pair_linear_residual(const AttnParams& p, const fl
 }
 
 template <int D, bool PROT, bool INJ, bool CAUSAL>
-__device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, float* ostage, uint64_t* s_full,
+__device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXch* xc, float* ostage,
+                                        const CUtensorMap* tm_o, uint64_t* s_full,
                                         uint64_t* s_free, uint64_t* p_ready, uint64_t* o_done, uint64_t* o_final,
                                         uint64_t* mx_early, uint64_t* mx_late, uint64_t* fin_bar, uint64_t* ack_bar,
                                         uint64_t* o_free, uint32_t tmem, int warp, int lane, int n,
@@ -712,7 +713,46 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     }
     if ((warp & 3) == 0) EFTA_TS(37, g_last);
     const size_t grow = static_cast<size_t>(seq_row0) + qt * kBlock + row;
-    {
+    if constexpr (D == 64) {
+        // asynchronous O store: the warp writes its 32 rows into its 8 KB staging buffer in
+        // the 128-byte-swizzled box layout (16-byte chunk c of row r at chunk c ^ (r & 7):
+        // conflict-free) and one lane hands it to the TMA engine, so warpgroup 1 leaves the
+        // epilogue without waiting for the stores (the d=64 epilogue sits on the max chain at
+        // every tile boundary). fp32 [BH*S, 64]: two 32-column boxes; fp16 token-major
+        // [B*S, H*64]: one 64-column box.
+        uint8_t* wbuf = reinterpret_cast<uint8_t*>(ostage) + wq * 8192;
+        if (lane == 0) bulk_wait_group_read0();  // this warp's previous tile store has read its buffer
+        __syncwarp();
+        const uint32_t sw = static_cast<uint32_t>(lane & 7);
+        if (p.o_tok) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                st_shared_v4(wbuf + lane * 128 + ((c ^ sw) << 4),
+                             make_uint4(pack_half2(o[8 * c], o[8 * c + 1]), pack_half2(o[8 * c + 2], o[8 * c + 3]),
+                                        pack_half2(o[8 * c + 4], o[8 * c + 5]), pack_half2(o[8 * c + 6], o[8 * c + 7])));
+        } else {
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    st_shared_v4(wbuf + b * 4096 + lane * 128 + ((c ^ sw) << 4),
+                                 make_uint4(__float_as_uint(o[32 * b + 4 * c]), __float_as_uint(o[32 * b + 4 * c + 1]),
+                                            __float_as_uint(o[32 * b + 4 * c + 2]), __float_as_uint(o[32 * b + 4 * c + 3])));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            if (p.o_tok) {
+                const int b = head / p.heads_q, h = head - b * p.heads_q;
+                tma_store_2d(tm_o, wbuf, h * 64, b * p.seq_len + qt * kBlock + wq * 32);
+            } else {
+                const int r0 = seq_row0 + qt * kBlock + wq * 32;
+                tma_store_2d(tm_o, wbuf, 0, r0);
+                tma_store_2d(tm_o, wbuf + 4096, 32, r0);
+            }
+            bulk_commit_group();
+        }
+    } else {
         // coalesced O store: thread = row holds D fp32; the warp stages 32 rows x 16 words at
         // a time through shared memory (16-byte chunks XOR-swizzled by row: conflict-free both
         // ways) and writes them back as full 64-byte row segments, 8 rows per instruction
@@ -772,7 +812,11 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     flush_families(fam_out);
     if ((warp & 3) == 0) EFTA_TS(39, g_last);
     }  // tiles
+    if constexpr (D == 64) {
+        if (w == 1 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // O stores done
+    }
     (void)MODE;
+    (void)tm_o;
 }
 
 }  // namespace efta_sm100

@@ -32,7 +32,7 @@ cudaError_t set_smem(K kern, uint32_t bytes) {
 
 template <int D, int MODE, bool INJ, bool CAUSAL = false>
 cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const CUtensorMap& tkb,
-                          const CUtensorMap& tkc, const CUtensorMap& tvt, const AttnParams& p, int bh,
+                          const CUtensorMap& tkc, const CUtensorMap& tvt, const CUtensorMap& tvo, const AttnParams& p, int bh,
                           cudaStream_t st) {
     using PL = PairLayout<D, MODE != 0>;
     auto kern = efta_attn_pair_kernel<D, MODE, INJ, CAUSAL>;
@@ -43,7 +43,7 @@ cudaError_t launch_pair_t(const CUtensorMap& tq, const CUtensorMap& tka, const C
     const int tiles = bh * (p.nblk / 2);  // (head, query pair) tiles
     const int ncl = std::min(tiles, std::max(1, nsm / 2));
     dim3 grid(2 * ncl);
-    kern<<<grid, kPairThreads, PL::SMEM_BYTES, st>>>(tq, tka, tkb, tkc, tvt, p);
+    kern<<<grid, kPairThreads, PL::SMEM_BYTES, st>>>(tq, tka, tkb, tkc, tvt, tvo, p);
     return cudaGetLastError();
 }
 
@@ -99,17 +99,17 @@ cudaError_t launch_encode_pair(bool prot, const void* k, const void* v, void* kc
 #if EFTA_INST_CAUSAL
 cudaError_t EFTA_CAT(efta_launch_attn_pair_causal, EFTA_SFX)(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                                             const CUtensorMap& tkb, const CUtensorMap& tkc,
-                                                            const CUtensorMap& tvt, const AttnParams& p, int bh,
+                                                            const CUtensorMap& tvt, const CUtensorMap& tvo, const AttnParams& p, int bh,
                                                             cudaStream_t st) {
-    return mode == 0 ? launch_pair_t<EFTA_INST_D, 0, false, true>(tq, tka, tkb, tkc, tvt, p, bh, st)
-                     : launch_pair_t<EFTA_INST_D, 2, false, true>(tq, tka, tkb, tkc, tvt, p, bh, st);
+    return mode == 0 ? launch_pair_t<EFTA_INST_D, 0, false, true>(tq, tka, tkb, tkc, tvt, tvo, p, bh, st)
+                     : launch_pair_t<EFTA_INST_D, 2, false, true>(tq, tka, tkb, tkc, tvt, tvo, p, bh, st);
 }
 #elif EFTA_INST_INJ
 cudaError_t EFTA_CAT(efta_launch_attn_pair_inj, EFTA_SFX)(const CUtensorMap& tq, const CUtensorMap& tka,
                                                          const CUtensorMap& tkb, const CUtensorMap& tkc,
-                                                         const CUtensorMap& tvt, const AttnParams& p, int bh,
+                                                         const CUtensorMap& tvt, const CUtensorMap& tvo, const AttnParams& p, int bh,
                                                          cudaStream_t st) {
-    return launch_pair_t<EFTA_INST_D, EFTA_MODE_EFTA_OPT, true>(tq, tka, tkb, tkc, tvt, p, bh, st);
+    return launch_pair_t<EFTA_INST_D, EFTA_MODE_EFTA_OPT, true>(tq, tka, tkb, tkc, tvt, tvo, p, bh, st);
 }
 #else
 cudaError_t EFTA_CAT(efta_launch_attn, EFTA_SFX)(int mode, bool dbg, const CUtensorMap& tq, const CUtensorMap& tk,
@@ -120,10 +120,10 @@ cudaError_t EFTA_CAT(efta_launch_attn, EFTA_SFX)(int mode, bool dbg, const CUten
 }
 cudaError_t EFTA_CAT(efta_launch_attn_pair, EFTA_SFX)(int mode, const CUtensorMap& tq, const CUtensorMap& tka,
                                                      const CUtensorMap& tkb, const CUtensorMap& tkc,
-                                                     const CUtensorMap& tvt, const AttnParams& p, int bh,
+                                                     const CUtensorMap& tvt, const CUtensorMap& tvo, const AttnParams& p, int bh,
                                                      cudaStream_t st) {
-    return mode == 0 ? launch_pair_t<EFTA_INST_D, 0, false>(tq, tka, tkb, tkc, tvt, p, bh, st)
-                     : launch_pair_t<EFTA_INST_D, 2, false>(tq, tka, tkb, tkc, tvt, p, bh, st);
+    return mode == 0 ? launch_pair_t<EFTA_INST_D, 0, false>(tq, tka, tkb, tkc, tvt, tvo, p, bh, st)
+                     : launch_pair_t<EFTA_INST_D, 2, false>(tq, tka, tkb, tkc, tvt, tvo, p, bh, st);
 }
 cudaError_t EFTA_CAT(efta_launch_encode_pair, EFTA_SFX)(bool prot, const void* k, const void* v, void* kc, void* vt,
                                                        int seq_len, int nblk, int bh, cudaStream_t st) {

@@ -56,8 +56,11 @@ struct PairLayout {
     static constexpr uint32_t RED_BYTES = 128 * 24 + 256;  // per row warpgroup
     static constexpr uint32_t OFF_XCH = OFF_RED + 2 * RED_BYTES;
     static constexpr uint32_t OFF_TINFO = OFF_XCH + 2 * 7168;  // chain exchange x tile parity; tile ring: int[4]
-    static constexpr uint32_t OFF_OSTG = OFF_TINFO + 16;       // epilogue O staging: 4 warps x 32 x 16 fp32
-    static constexpr uint32_t SMEM_BYTES = OFF_OSTG + 4 * 2048 + 1024;
+    // epilogue O staging: d=64 holds each warp's 32 output rows (8 KB, 128-byte swizzle) for an
+    // asynchronous TMA store; d=128 (no room) stages 32 x 16 fp32 chunks for coalesced stores
+    static constexpr uint32_t OSTG_BYTES = D == 64 ? 4 * 8192 : 4 * 2048;
+    static constexpr uint32_t OFF_OSTG = D == 64 ? ((OFF_TINFO + 16 + 1023) & ~1023u) : OFF_TINFO + 16;
+    static constexpr uint32_t SMEM_BYTES = OFF_OSTG + OSTG_BYTES + 1024;
     // TMEM columns
     static constexpr uint32_t COL_S0 = 0, COL_O = 2 * SW, COL_P = COL_O + VROWS, TMEM_COLS = 512;
     // one P buffer per row warpgroup when it fits (unprotected d=128, every d=64 variant);
@@ -137,7 +140,8 @@ template <int D, int MODE, bool INJ, bool CAUSAL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_ka,
                       const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_kc,
-                      const __grid_constant__ CUtensorMap tm_vt, const AttnParams p) {
+                      const __grid_constant__ CUtensorMap tm_vt, const __grid_constant__ CUtensorMap tm_o,
+                      const AttnParams p) {
     constexpr bool PROT = MODE != EFTA_MODE_NONE;
     using L = PairLayout<D, PROT>;
     constexpr int KS = L::KS, VS = L::VS, NSUB = L::NSUB;
@@ -390,7 +394,7 @@ efta_attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_con
     } else {
         setmaxnreg_inc<232>();
         row_alt<D, PROT, INJ, CAUSAL>(p, smem + L::OFF_RED, reinterpret_cast<AltXch*>(smem + L::OFF_XCH),
-                              reinterpret_cast<float*>(smem + L::OFF_OSTG), s_full,
+                              reinterpret_cast<float*>(smem + L::OFF_OSTG), &tm_o, s_full,
                               s_free, p_ready, o_done, o_final, mx_early, mx_late, fin_bar, ack_bar, o_free, tmem,
                               warp, lane, n, tinfo, t_full, t_empty, rank);
     }

@@ -80,6 +80,21 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// the d=64 pair kernel's output map (TMA store, 128-byte swizzle, boxes of 32 rows): fp32
+// [rows, 64] in 32-column boxes, or fp16 [rows, cols] (token-major) in 64-column boxes
+bool make_out_map(CUtensorMap* m, void* base, bool f16, uint64_t rows, uint64_t cols) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const uint64_t esz = f16 ? 2 : 4;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * esz};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), 32};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box,
+              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int validate(const efta_attn_desc* d) {
     if (!d) return fail(1, "efta: null descriptor");
     // reference AttnConfig::validate (include/efta/config.hpp:30-41)
@@ -305,6 +320,12 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
             tvc = tq;
         }
     }
+    CUtensorMap to = tq;  // d=64 pair kernel: the TMA-stored output
+    if (ok && pair && D == 64)
+        ok = d->o_token_major
+                 ? make_out_map(&to, o, true, static_cast<uint64_t>(d->batch) * d->seq_len,
+                                static_cast<uint64_t>(d->heads) * D)
+                 : make_out_map(&to, o, false, rows, D);
     if (!ok) return fail(2, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
     AttnParams p{};
@@ -351,14 +372,14 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
     if (pair)  // the persistent pair kernel's in-order tile counter (workspace scratch, int)
         CUDA_TRY(cudaMemsetAsync(wsb + wl.scratch, 0, 16, st));
     if (pair && dbg)  // the tap build: maps as below
-        e = (D == 64) ? efta_launch_attn_pair_inj_d64(tq, tk, tv, tkc, tvc, p, bh, st)
-                      : efta_launch_attn_pair_inj_d128(tq, tk, tv, tkc, tvc, p, bh, st);
+        e = (D == 64) ? efta_launch_attn_pair_inj_d64(tq, tk, tv, tkc, tvc, to, p, bh, st)
+                      : efta_launch_attn_pair_inj_d128(tq, tk, tv, tkc, tvc, to, p, bh, st);
     else if (pair && d->causal)
-        e = (D == 64) ? efta_launch_attn_pair_causal_d64(d->mode, tq, tk, tv, tkc, tvc, p, bh, st)
-                      : efta_launch_attn_pair_causal_d128(d->mode, tq, tk, tv, tkc, tvc, p, bh, st);
+        e = (D == 64) ? efta_launch_attn_pair_causal_d64(d->mode, tq, tk, tv, tkc, tvc, to, p, bh, st)
+                      : efta_launch_attn_pair_causal_d128(d->mode, tq, tk, tv, tkc, tvc, to, p, bh, st);
     else if (pair)  // maps: q, K half A, K half B (protected peer), KC, [V^T ; VC^T]
-        e = (D == 64) ? efta_launch_attn_pair_d64(d->mode, tq, tk, tv, tkc, tvc, p, bh, st)
-                      : efta_launch_attn_pair_d128(d->mode, tq, tk, tv, tkc, tvc, p, bh, st);
+        e = (D == 64) ? efta_launch_attn_pair_d64(d->mode, tq, tk, tv, tkc, tvc, to, p, bh, st)
+                      : efta_launch_attn_pair_d128(d->mode, tq, tk, tv, tkc, tvc, to, p, bh, st);
     else
         e = (D == 64) ? efta_launch_attn_d64(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st)
                       : efta_launch_attn_d128(d->mode, dbg, tq, tk, tv, tkc, tvc, p, bh, st);
