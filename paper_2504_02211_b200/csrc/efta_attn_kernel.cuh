@@ -283,6 +283,59 @@ __device__ __forceinline__ void row_sums(const float (&o)[D], float (&s1)[kStrid
     }
 }
 
+// Final output check (efta.cpp:329-336) of the tile, thread = row. pre_bad / pre: a per-row
+// condition decided before (the rowsum range restriction of the CTA-pair kernel) whose tile
+// event the reference emits first; it shares the common-case barrier with the output check
+// (one warpgroup barrier for a clean tile), and `pre` runs warpgroup-wide only if some row has it.
+template <int D, typename Pre>
+__device__ __forceinline__ void verify_output_tile_pre(const AttnParams& p, float (&o)[D],
+                                                       const float (&c1)[kStride],
+                                                       const float (&c2)[kStride], double eps_row,
+                                                       int head, int bi, int bj, int row,
+                                                       const RowScratch& rs, float& residual_out,
+                                                       uint32_t bo, bool pre_bad, Pre&& pre) {
+    constexpr int G = D / kStride;
+    float s1[kStride], s2[kStride];
+    row_sums<D>(o, s1, s2);
+    bool viol = false, cs_bad = false;
+    double res = 0.0;
+#pragma unroll
+    for (int x = 0; x < kStride; ++x) {
+        cs_bad |= !isfinite(c1[x]) || !isfinite(c2[x]);
+        if (!isfinite(s1[x]) || !isfinite(s2[x])) { viol = true; continue; }
+        const double d1 = static_cast<double>(c1[x]) - s1[x];
+        const double d2 = static_cast<double>(c2[x]) - s2[x];
+        res = fmax(res, fmax(fabs(d1), fabs(d2) / G));
+        viol |= (fabs(d1) > eps_row) || (fabs(d2) > eps_row * G);
+    }
+    residual_out = static_cast<float>(res);
+    if (!named_bar_or(5 + bo, 128, viol || cs_bad || pre_bad)) return;
+    if (named_bar_or(7 + bo, 128, pre_bad)) pre();
+    const bool tile_cs_bad = named_bar_or(4 + bo, 128, cs_bad);
+    const bool any = named_bar_or(5 + bo, 128, viol || cs_bad);
+    if (!any) return;
+    RowVerify rv{};
+    rv.best_col = -1;
+    rv.restored_col = -1;
+    rv.residual = res;
+    if (!tile_cs_bad && viol) {
+        float t[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) t[c] = o[c];
+        float cc1[kStride], cc2[kStride];
+#pragma unroll
+        for (int x = 0; x < kStride; ++x) { cc1[x] = c1[x]; cc2[x] = c2[x]; }
+        verify_row<D>(t, cc1, cc2, eps_row, rv);
+#pragma unroll
+        for (int c = 0; c < D; ++c) o[c] = t[c];
+        residual_out = static_cast<float>(rv.residual);
+    }
+    TileReport tr = reduce_tile_report(rv, tile_cs_bad, row, rs.slots, rs.ints, rs.dbl, bo);
+    if (row == 0)
+        push_event(p, EFTA_OUTPUT_CHECKSUM, head, bi, bj, tr.status, tr.row, tr.col, tr.violations,
+                   tr.corrections, tr.checksum_repair, tr.residual, tr.delta);
+}
+
 template <int D>
 __device__ __forceinline__ void verify_output_tile(const AttnParams& p, float (&o)[D],
                                                    const float (&c1)[kStride],
@@ -329,8 +382,6 @@ __device__ __forceinline__ void verify_output_tile(const AttnParams& p, float (&
         push_event(p, EFTA_OUTPUT_CHECKSUM, head, bi, bj, tr.status, tr.row, tr.col, tr.violations,
                    tr.corrections, tr.checksum_repair, tr.residual, tr.delta);
 }
-
-
 
 template <bool PAIR>
 __device__ __forceinline__ void signal_p_ready(uint64_t* bar, int lane) {
