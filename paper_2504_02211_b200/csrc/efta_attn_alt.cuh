@@ -764,57 +764,52 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             bulk_commit_group();
         }
     } else {
-        // coalesced O store: thread = row holds D fp32; the warp stages 32 rows x 16 words at
-        // a time through shared memory (16-byte chunks XOR-swizzled by row: conflict-free both
-        // ways) and writes them back as full 64-byte row segments, 8 rows per instruction
-        // (a row per thread made every 16-byte store touch 32 lines: an LSU-bound epilogue).
-        // A word is one fp32 value ([BH, S, D] output) or two fp16 values (token-major
-        // [B, S, H, D] output: row r of the warp lands at token b*S + s, head column h*D).
-        uint32_t* stg = reinterpret_cast<uint32_t*>(ostage) + wq * 512;
-        uint8_t* obase;  // row 0 of this warp
-        size_t opitch;
+        // d=128: the same asynchronous store in 16-row boxes (32 rows x 512 bytes per warp do not
+        // fit next to the K / V rings): box (rh, cb) = rows 16 rh.. of the warp, 128-byte column
+        // block cb, staged through L::OBUF_N 2 KB buffers per warp; a buffer is rewritten once
+        // the TMA engine has read it (wait_group.read OBUF_N - 1)
+        constexpr int NB = L::OBUF_N;
+        uint8_t* wb = reinterpret_cast<uint8_t*>(ostage) + wq * NB * 2048;
+        const uint32_t sw = static_cast<uint32_t>(lane & 7);
+        uint8_t* rowp0 = wb + (lane & 15) * 128;
+        // box kb: wait for its buffer, the rows' 8 chunks (lanes of row half rh), TMA store
+        auto box = [&](int kb, int rh, int col, int grow0, auto chunk) {
+            if (lane == 0) bulk_wait_group_read<NB - 1>();
+            __syncwarp();
+            if ((lane >> 4) == rh) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) st_shared_v4(rowp0 + (kb % NB) * 2048 + ((c ^ sw) << 4), chunk(c));
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(tm_o, wb + (kb % NB) * 2048, col, grow0 + 16 * rh);
+                bulk_commit_group();
+            }
+        };
         if (p.o_tok) {
             const int b = head / p.heads_q, h = head - b * p.heads_q;
-            const size_t tok0 = static_cast<size_t>(b) * p.seq_len + qt * kBlock + row - lane;
-            obase = reinterpret_cast<uint8_t*>(p.o) + ((tok0 * p.heads_q + h) * D) * 2;
-            opitch = static_cast<size_t>(p.heads_q) * D * 2;
+            const int t0 = b * p.seq_len + qt * kBlock + wq * 32;
+#pragma unroll
+            for (int rh = 0; rh < 2; ++rh)
+#pragma unroll
+                for (int cb = 0; cb < 2; ++cb)
+                    box(rh * 2 + cb, rh, h * 128 + 64 * cb, t0, [&](int c) {
+                        const int b0 = 64 * cb + 8 * c;
+                        return make_uint4(pack_half2(o[b0], o[b0 + 1]), pack_half2(o[b0 + 2], o[b0 + 3]),
+                                          pack_half2(o[b0 + 4], o[b0 + 5]), pack_half2(o[b0 + 6], o[b0 + 7]));
+                    });
         } else {
-            obase = reinterpret_cast<uint8_t*>(p.o + (grow - lane) * D);
-            opitch = D * 4;
-        }
-        auto put = [&](int q4, uint4 w4) {
-            *reinterpret_cast<uint4*>(stg + lane * 16 + ((q4 ^ (lane & 3)) << 2)) = w4;
-        };
-        auto flush = [&](int c) {  // the staged 32 x 64-byte block -> 64-byte segment c of each row
-            __syncwarp();
+            const int r0 = seq_row0 + qt * kBlock + wq * 32;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int r = 8 * i + (lane >> 2), q4 = lane & 3;
-                const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 16 + ((q4 ^ (r & 3)) << 2));
-                *reinterpret_cast<uint4*>(obase + static_cast<size_t>(r) * opitch + c * 64 + 16 * q4) = v;
-            }
-            __syncwarp();
-        };
-        if (p.o_tok) {
+            for (int rh = 0; rh < 2; ++rh)
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-#pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    const int b0 = c * 32 + 8 * q4;
-                    put(q4, make_uint4(pack_half2(o[b0], o[b0 + 1]), pack_half2(o[b0 + 2], o[b0 + 3]),
-                                       pack_half2(o[b0 + 4], o[b0 + 5]), pack_half2(o[b0 + 6], o[b0 + 7])));
-                }
-                flush(c);
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < D / 16; ++c) {
-#pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4)
-                    put(q4, make_uint4(__float_as_uint(o[c * 16 + 4 * q4]), __float_as_uint(o[c * 16 + 4 * q4 + 1]),
-                                       __float_as_uint(o[c * 16 + 4 * q4 + 2]), __float_as_uint(o[c * 16 + 4 * q4 + 3])));
-                flush(c);
-            }
+                for (int cb = 0; cb < 4; ++cb)
+                    box(rh * 4 + cb, rh, 32 * cb, r0, [&](int c) {
+                        const int b0 = 32 * cb + 4 * c;
+                        return make_uint4(__float_as_uint(o[b0]), __float_as_uint(o[b0 + 1]), __float_as_uint(o[b0 + 2]),
+                                          __float_as_uint(o[b0 + 3]));
+                    });
         }
     }
     if (p.m_out) p.m_out[grow] = m_run;
@@ -823,9 +818,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     flush_families(fam_out);
     if ((warp & 3) == 0) EFTA_TS(39, g_last);
     }  // tiles
-    if constexpr (D == 64) {
-        if (w == 1 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // O stores done
-    }
+    if (w == 1 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // O stores done
     (void)MODE;
     (void)tm_o;
 }

@@ -57,9 +57,11 @@ struct PairLayout {
     static constexpr uint32_t OFF_XCH = OFF_RED + 2 * RED_BYTES;
     static constexpr uint32_t OFF_TINFO = OFF_XCH + 2 * 7168;  // chain exchange x tile parity; tile ring: int[4]
     // epilogue O staging: d=64 holds each warp's 32 output rows (8 KB, 128-byte swizzle) for an
-    // asynchronous TMA store; d=128 (no room) stages 32 x 16 fp32 chunks for coalesced stores
-    static constexpr uint32_t OSTG_BYTES = D == 64 ? 4 * 8192 : 4 * 2048;
-    static constexpr uint32_t OFF_OSTG = D == 64 ? ((OFF_TINFO + 16 + 1023) & ~1023u) : OFF_TINFO + 16;
+    // asynchronous TMA store; d=128 stages 16-row boxes through two (protected) or one 2 KB
+    // buffer per warp (what the K / V rings leave)
+    static constexpr int OBUF_N = D == 64 ? 4 : (PROT ? 2 : 1);  // per warp: 2 KB buffers
+    static constexpr uint32_t OSTG_BYTES = 4 * 2048 * OBUF_N;
+    static constexpr uint32_t OFF_OSTG = (OFF_TINFO + 16 + 1023) & ~1023u;
     static constexpr uint32_t SMEM_BYTES = OFF_OSTG + OSTG_BYTES + 1024;
     // TMEM columns
     static constexpr uint32_t COL_S0 = 0, COL_O = 2 * SW, COL_P = COL_O + VROWS, TMEM_COLS = 512;

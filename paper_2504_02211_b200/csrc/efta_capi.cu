@@ -80,15 +80,15 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// the d=64 pair kernel's output map (TMA store, 128-byte swizzle, boxes of 32 rows): fp32
-// [rows, 64] in 32-column boxes, or fp16 [rows, cols] (token-major) in 64-column boxes
-bool make_out_map(CUtensorMap* m, void* base, bool f16, uint64_t rows, uint64_t cols) {
+// the pair kernel's output map (TMA store, 128-byte swizzle): fp32 [rows, d] in 32-column boxes,
+// or fp16 [rows, cols] (token-major) in 64-column boxes
+bool make_out_map(CUtensorMap* m, void* base, bool f16, uint64_t rows, uint64_t cols, uint32_t box_rows) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     const uint64_t esz = f16 ? 2 : 4;
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {cols * esz};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), 32};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box,
               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -320,12 +320,12 @@ int efta_attn_fwd_f16(const efta_attn_desc* d, const uint16_t* q, const uint16_t
             tvc = tq;
         }
     }
-    CUtensorMap to = tq;  // d=64 pair kernel: the TMA-stored output
-    if (ok && pair && D == 64)
+    CUtensorMap to = tq;  // pair kernel: the TMA-stored output (boxes of 32 rows at d=64, 16 at d=128)
+    if (ok && pair)
         ok = d->o_token_major
                  ? make_out_map(&to, o, true, static_cast<uint64_t>(d->batch) * d->seq_len,
-                                static_cast<uint64_t>(d->heads) * D)
-                 : make_out_map(&to, o, false, rows, D);
+                                static_cast<uint64_t>(d->heads) * D, D == 64 ? 32 : 16)
+                 : make_out_map(&to, o, false, rows, D, D == 64 ? 32 : 16);
     if (!ok) return fail(2, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
     AttnParams p{};
