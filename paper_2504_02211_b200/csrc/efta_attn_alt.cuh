@@ -114,6 +114,9 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     static_assert(!INJ || PROT, "the fault-tap build is the protected variant");
     constexpr int MODE = PROT ? EFTA_MODE_EFTA_OPT : EFTA_MODE_NONE;
     constexpr bool kWideTmem = (!PROT || D == 64) && !INJ;
+    // d=128 O store: the coalesced staged stores (default) or 16-row TMA boxes (A/B: +2% at S=2048,
+    // -0.4% at C4 and -1.5% causal, profiles/r02/ab_d128_tma_ostore.log)
+    constexpr bool kTmaStore128 = EFTA_TMA_STORE_D128 != 0;
     const int w = (warp - 4) >> 2;
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
@@ -763,8 +766,61 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
             }
             bulk_commit_group();
         }
+    } else if constexpr (!kTmaStore128) {
+        // coalesced O store: thread = row holds D fp32; the warp stages 32 rows x 16 words at
+        // a time through shared memory (16-byte chunks XOR-swizzled by row: conflict-free both
+        // ways) and writes them back as full 64-byte row segments, 8 rows per instruction
+        // (a row per thread made every 16-byte store touch 32 lines: an LSU-bound epilogue).
+        // A word is one fp32 value ([BH, S, D] output) or two fp16 values (token-major
+        // [B, S, H, D] output: row r of the warp lands at token b*S + s, head column h*D).
+        uint32_t* stg = reinterpret_cast<uint32_t*>(ostage) + wq * 512;
+        uint8_t* obase;  // row 0 of this warp
+        size_t opitch;
+        if (p.o_tok) {
+            const int b = head / p.heads_q, h = head - b * p.heads_q;
+            const size_t tok0 = static_cast<size_t>(b) * p.seq_len + qt * kBlock + row - lane;
+            obase = reinterpret_cast<uint8_t*>(p.o) + ((tok0 * p.heads_q + h) * D) * 2;
+            opitch = static_cast<size_t>(p.heads_q) * D * 2;
+        } else {
+            obase = reinterpret_cast<uint8_t*>(p.o + (grow - lane) * D);
+            opitch = D * 4;
+        }
+        auto put = [&](int q4, uint4 w4) {
+            *reinterpret_cast<uint4*>(stg + lane * 16 + ((q4 ^ (lane & 3)) << 2)) = w4;
+        };
+        auto flush = [&](int c) {  // the staged 32 x 64-byte block -> 64-byte segment c of each row
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = 8 * i + (lane >> 2), q4 = lane & 3;
+                const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 16 + ((q4 ^ (r & 3)) << 2));
+                *reinterpret_cast<uint4*>(obase + static_cast<size_t>(r) * opitch + c * 64 + 16 * q4) = v;
+            }
+            __syncwarp();
+        };
+        if (p.o_tok) {
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const int b0 = c * 32 + 8 * q4;
+                    put(q4, make_uint4(pack_half2(o[b0], o[b0 + 1]), pack_half2(o[b0 + 2], o[b0 + 3]),
+                                       pack_half2(o[b0 + 4], o[b0 + 5]), pack_half2(o[b0 + 6], o[b0 + 7])));
+                }
+                flush(c);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < D / 16; ++c) {
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4)
+                    put(q4, make_uint4(__float_as_uint(o[c * 16 + 4 * q4]), __float_as_uint(o[c * 16 + 4 * q4 + 1]),
+                                       __float_as_uint(o[c * 16 + 4 * q4 + 2]), __float_as_uint(o[c * 16 + 4 * q4 + 3])));
+                flush(c);
+            }
+        }
     } else {
-        // d=128: the same asynchronous store in 16-row boxes (32 rows x 512 bytes per warp do not
+        // (EFTA_TMA_STORE_D128=1 builds) d=128: the same asynchronous store in 16-row boxes (32 rows x 512 bytes per warp do not
         // fit next to the K / V rings): box (rh, cb) = rows 16 rh.. of the warp, 128-byte column
         // block cb, staged through L::OBUF_N 2 KB buffers per warp; a buffer is rewritten once
         // the TMA engine has read it (wait_group.read OBUF_N - 1)

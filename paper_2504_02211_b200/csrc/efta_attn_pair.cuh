@@ -27,6 +27,10 @@
 #pragma once
 #include "efta_attn_kernel.cuh"
 
+#ifndef EFTA_TMA_STORE_D128
+#define EFTA_TMA_STORE_D128 0  // d=128 O store through 16-row TMA boxes (A/B variant, default off)
+#endif
+
 namespace efta_sm100 {
 
 template <int D, bool PROT>
@@ -59,9 +63,12 @@ struct PairLayout {
     // epilogue O staging: d=64 holds each warp's 32 output rows (8 KB, 128-byte swizzle) for an
     // asynchronous TMA store; d=128 stages 16-row boxes through two (protected) or one 2 KB
     // buffer per warp (what the K / V rings leave)
-    static constexpr int OBUF_N = D == 64 ? 4 : (PROT ? 2 : 1);  // per warp: 2 KB buffers
+    // (the d=128 TMA variant, EFTA_TMA_STORE_D128=1, needs 1 KB-aligned buffers: two per warp
+    // protected, one unprotected; the default d=128 build keeps the coalesced path's 2 KB per warp)
+    static constexpr bool kTma = D == 64 || EFTA_TMA_STORE_D128 != 0;
+    static constexpr int OBUF_N = D == 64 ? 4 : ((EFTA_TMA_STORE_D128 != 0 && PROT) ? 2 : 1);  // per warp: 2 KB buffers
     static constexpr uint32_t OSTG_BYTES = 4 * 2048 * OBUF_N;
-    static constexpr uint32_t OFF_OSTG = (OFF_TINFO + 16 + 1023) & ~1023u;
+    static constexpr uint32_t OFF_OSTG = kTma ? ((OFF_TINFO + 16 + 1023) & ~1023u) : OFF_TINFO + 16;
     static constexpr uint32_t SMEM_BYTES = OFF_OSTG + OSTG_BYTES + 1024;
     // TMEM columns
     static constexpr uint32_t COL_S0 = 0, COL_O = 2 * SW, COL_P = COL_O + VROWS, TMEM_COLS = 512;

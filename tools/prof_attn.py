@@ -20,12 +20,13 @@ ap.add_argument("--d", type=int, default=128)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--tok", action="store_true", help="fp16 token-major O output")
+ap.add_argument("--causal", action="store_true")
 a = ap.parse_args()
 shape = (a.b, a.h, a.s, a.d)
 q = torch.empty(shape, device="cuda").uniform_(-1, 1).half()
 k = torch.empty(shape, device="cuda").uniform_(-1, 1).half()
 v = torch.empty(shape, device="cuda").uniform_(-1, 1).half()
-op = EftaAttention(*shape, mode=a.mode, thr=Thresholds(1e-4, 1e-3, 1e-3), token_major_out=a.tok)
+op = EftaAttention(*shape, mode=a.mode, thr=Thresholds(1e-4, 1e-3, 1e-3), token_major_out=a.tok, causal=a.causal)
 for _ in range(a.iters):
     op(q, k, v)
 torch.cuda.synchronize()
@@ -38,4 +39,5 @@ if a.time:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
-    print(f"{a.mode}{' tok' if a.tok else ''} {shape}: {ms:.3f} ms  {4*a.b*a.h*a.s*a.s*a.d/ms/1e9:.1f} TFLOP/s  det={op.report().detections}")
+    fl = (2 if a.causal else 4) * a.b * a.h * a.s * a.s * a.d
+    print(f"{a.mode}{' tok' if a.tok else ''}{' causal' if a.causal else ''} {shape}: {ms:.3f} ms  {fl/ms/1e9:.1f} TFLOP/s  det={op.report().detections}")
