@@ -302,16 +302,29 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                 for (int x = 0; x < 128; ++x)
                     if (x == f_col - half * 128) v[x] = __uint_as_float(__float_as_uint(v[x]) ^ (1u << f_bit));
             }
-            bool nonfin = false;
+            // strided sums in the reference order (ascending l, multiply then add), two groups
+            // per packed f32x2 instruction: per lane the same rounded ops as the scalar form.
+            // A non-finite value makes its group's sum non-finite, so the verification below
+            // flags it without a per-element test (c1 - s1 is then non-finite).
+            {
+                float2 s1p[4], s2p[4];
 #pragma unroll
-            for (int l = 0; l < 16; ++l) {
-                const float w = static_cast<float>(half * 16 + l + 1);
+                for (int q = 0; q < 4; ++q) { s1p[q] = make_float2(0.0f, 0.0f); s2p[q] = s1p[q]; }
 #pragma unroll
-                for (int x = 0; x < 8; ++x) {
-                    const float val = v[l * 8 + x];
-                    s1[x] = __fadd_rn(s1[x], val);
-                    s2[x] = __fadd_rn(s2[x], __fmul_rn(w, val));
-                    nonfin |= !isfinite(val);
+                for (int l = 0; l < 16; ++l) {
+                    const float w = static_cast<float>(half * 16 + l + 1);
+                    const float2 w2 = make_float2(w, w);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float2 val = make_float2(v[l * 8 + 2 * q], v[l * 8 + 2 * q + 1]);
+                        s1p[q] = fadd2(s1p[q], val);
+                        s2p[q] = fadd2(s2p[q], fmul2(w2, val));
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    s1[2 * q] = s1p[q].x; s1[2 * q + 1] = s1p[q].y;
+                    s2[2 * q] = s2p[q].x; s2[2 * q + 1] = s2p[q].y;
                 }
             }
             // this half's output row segment (fp16 or fp32), stored once the accumulator is
@@ -407,7 +420,7 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
             tmem_ld16(lb + 272, lo);
             tmem_wait_ld();
             float c1[8], c2[8];
-            bool viol = nonfin, cs_bad = false;
+            bool viol = false, cs_bad = false;
             double res = 0.0;
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
@@ -428,8 +441,9 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
                 cs[2] = make_float4(c2[0], c2[1], c2[2], c2[3]);
                 cs[3] = make_float4(c2[4], c2[5], c2[6], c2[7]);
             }
-            const bool tile_cs_bad = named_bar_or(4, 128, cs_bad);
+            // one warpgroup barrier decides a clean tile; the checksum-health vote only on the rare path
             const bool any = named_bar_or(5, 128, viol || cs_bad);
+            const bool tile_cs_bad = any && named_bar_or(4, 128, cs_bad);
             if (row == 0) *dec = any ? 1 : 0;
             named_bar_arrive(7, 256);
             if (!any) {
