@@ -102,3 +102,37 @@ def test_pair_and_single_cta_kernels_agree(m, monkeypatch):
         outs.append((y.float().cpu().numpy(), lin.report().detections))
     assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
     assert outs[0][1] == outs[1][1] == 0
+
+
+def test_nonfinite_accumulator_flagged_like_oracle(problem):
+    """A bit-30 upset of a cell in [1, 2) makes it inf / NaN (exponent 0x7f -> 0xff). The epilogue
+    has no per-element finiteness test: the non-finite cell makes its group's strided sum
+    non-finite, which fails the check. Status per tile must equal the oracle's verify_locate_correct
+    on the same corrupted tile (src/abft.cpp:65-187)."""
+    from paper_2504_02211_b200.ffn import AbftLinear
+    x, w, xt, wt, tiles = problem
+    orc = oracle()
+    clean = AbftLinear(wt, eps=EPS)
+    y0 = clean(xt).float().cpu().numpy()
+    faults = []
+    for mt in range(M // 128):
+        for nt in range(N // 256):
+            blk = np.abs(y0[mt * 128:(mt + 1) * 128, nt * 256:(nt + 1) * 256])
+            rr, cc = np.nonzero((blk >= 1.01) & (blk < 1.99))  # away from the exponent edges
+            if len(rr):
+                faults.append((mt * 128 + int(rr[0]), nt * 256 + int(cc[0]), 30))
+    assert faults, "no accumulator value in [1, 2)"
+    lin = AbftLinear(wt, eps=EPS, debug=True)
+    lin.set_faults(faults)
+    lin(xt)
+    rep = lin.report()
+    for (r, c, b) in faults:
+        t = c // 256
+        cm, c1, c2 = tiles[t]
+        ct = cm.copy()
+        ct[r, c % 256] = orc.flip_bit(float(ct[r, c % 256]), 32, b)
+        assert not np.isfinite(ct[r, c % 256])
+        ro = orc.verify_locate_correct(ct, c1, c2, EPS)
+        ev = [e for e in rep.events if e["m_tile"] == r // 128 and e["n_tile"] == t]
+        assert ev and ro["status"] != "clean", (r, c, ro)
+        assert ev[0]["status"] == ro["status"], (ev[0], ro)
