@@ -426,13 +426,8 @@ abft_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant
             for (int x = 0; x < 8; ++x) {
                 c1[x] = __fadd_rn(__uint_as_float(hi[x]), __uint_as_float(lo[x]));
                 c2[x] = __fadd_rn(__uint_as_float(hi[8 + x]), __uint_as_float(lo[8 + x]));
-                cs_bad |= !isfinite(c1[x]) || !isfinite(c2[x]);
-                const double d1 = static_cast<double>(c1[x]) - s1[x];
-                const double d2 = static_cast<double>(c2[x]) - s2[x];
-                if (!isfinite(d1) || !isfinite(d2)) { viol = true; continue; }
-                res = fmax(res, fmax(fabs(d1), fabs(d2) / 32.0));
-                viol |= fabs(d1) > p.eps || fabs(d2) > p.eps * 32.0;
             }
+            group_check<8, 32, true>(c1, c2, s1, s2, p.eps, viol, cs_bad, res);
             fam = fmaxf(fam, static_cast<float>(res));
             if (p.ycs) {
                 float4* cs = reinterpret_cast<float4*>(p.ycs + (static_cast<size_t>(grow) * p.n_tiles + nt) * 16);

@@ -106,9 +106,17 @@ __device__ __forceinline__ int kv_head(const AttnParams& p, int head) {
             (threadIdx.x & 31) == 0 && (j) >= 0 && (j) < 64)                                   \
             p.prof[(j) * 64 + 16 + (base) + ((threadIdx.x >> 5) & 3)] = clock64();              \
     } while (0)
+// per warp quarter of the calling warpgroup (lane 0 of each warp): slots base .. base + 3
+#define EFTA_TSW(base, j)                                                                      \
+    do {                                                                                       \
+        if (p.prof && blockIdx.x == 2 && blockIdx.y == (gridDim.y > 1 ? 5 : 0) &&             \
+            (threadIdx.x & 31) == 0 && (j) >= 0 && (j) < 64)                                   \
+            p.prof[(j) * 64 + (base) + ((threadIdx.x >> 5) & 3)] = clock64();                  \
+    } while (0)
 #else
 #define EFTA_TS(slot, j) do { } while (0)
 #define EFTA_TSQ(base, j) do { } while (0)
+#define EFTA_TSW(base, j) do { } while (0)
 #endif
 
 
@@ -267,6 +275,45 @@ __device__ __forceinline__ void push_event(const AttnParams& p, int kind, int he
 // its 2x8 checksums live in this thread). Operates on a local array (only used
 // on the slow path). The caller handles the tile-wide "checksum non-finite"
 // early return (abft.cpp:74-78).
+// The strided group check of one row against its checksums with the reference's double
+// residuals (|c1 - s1| > eps or |c2 - s2| > eps * G flags the row; residual max(|d1|, |d2| / G)),
+// behind an fp32 screen: when every difference is finite and below both thresholds by a 2^-12
+// margin, the double test passes too, and the fp32 residual equals the double one rounded once
+// (fsub is the correctly rounded exact difference, G a power of two), so a clean row skips the
+// double arithmetic (measured ~1200-1700 clk per d=64 tile epilogue, on the max chain). Any other
+// row runs the double path unchanged. FIN_ON_D: a non-finite sum is judged on the difference (the
+// GEMM epilogue) rather than on the sums (attention); both flag the row.
+template <int NG, int G, bool FIN_ON_D>
+__device__ __forceinline__ void group_check(const float (&c1)[NG], const float (&c2)[NG], const float (&s1)[NG],
+                                            const float (&s2)[NG], double eps, bool& viol, bool& cs_bad,
+                                            double& res) {
+    static_assert((G & (G - 1)) == 0, "G must be a power of two (exact residual scaling)");
+    const float e1 = static_cast<float>(eps * (1.0 - 0x1p-12));
+    const float e2 = static_cast<float>(eps * G * (1.0 - 0x1p-12));
+    bool fast = true;
+    float rf = 0.0f;
+#pragma unroll
+    for (int x = 0; x < NG; ++x) {
+        const float a = fabsf(__fsub_rn(c1[x], s1[x])), b = fabsf(__fsub_rn(c2[x], s2[x]));
+        fast = fast && a <= e1 && b <= e2;  // false for NaN / inf differences
+        rf = fmaxf(rf, fmaxf(a, b * (1.0f / G)));
+    }
+    if (fast) {
+        res = fmax(res, static_cast<double>(rf));
+        return;
+    }
+#pragma unroll
+    for (int x = 0; x < NG; ++x) {
+        cs_bad |= !isfinite(c1[x]) || !isfinite(c2[x]);
+        if (!FIN_ON_D && (!isfinite(s1[x]) || !isfinite(s2[x]))) { viol = true; continue; }
+        const double d1 = static_cast<double>(c1[x]) - s1[x];
+        const double d2 = static_cast<double>(c2[x]) - s2[x];
+        if (FIN_ON_D && (!isfinite(d1) || !isfinite(d2))) { viol = true; continue; }
+        res = fmax(res, fmax(fabs(d1), fabs(d2) / G));
+        viol |= (fabs(d1) > eps) || (fabs(d2) > eps * G);
+    }
+}
+
 struct RowVerify {
     int violations, corrections, checksum_repair, uncorrectable, nonfinite;
     int restored_col;      // last erasure-restored column (-1 none)

@@ -629,6 +629,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     __syncwarp();
     if (lane == 0) mbar_arrive_cluster(o_free, 0);
     if ((warp & 3) == 0) EFTA_TS(35, g_last);
+    EFTA_TSW(52, g_last);
     if constexpr (INJ) tap_row<D>(tap, p, EFTA_GEMM2_ACC, n - 1, o);
     {
         // bring O, its checksums, l and the lower bound from the lazy reference max to
@@ -693,6 +694,7 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
         if (PROT && named_bar_or(7 + bo, 128, range_bad)) range_event();
     }
     if ((warp & 3) == 0) EFTA_TS(36, g_last);
+    EFTA_TSW(56, g_last);
     // normalization (efta.cpp:312-327): one IEEE reciprocal, then products (within 1 ulp of
     // the reference's division); the tap build keeps the reference's division [NORMALIZE_OUT]
     if constexpr (INJ) {
@@ -716,11 +718,12 @@ __device__ __forceinline__ void row_alt(const AttnParams& p, uint8_t* red, AltXc
     }
     float fam_out = 0.0f;
     if ((warp & 3) == 0) EFTA_TS(40, g_last);
+    EFTA_TSW(48, g_last);
     if (PROT) {
         float res;
         if constexpr (D == 64)  // one warpgroup barrier for a clean tile (+2% at S=512, d=64)
             verify_output_tile_pre<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res, bo, range_bad,
-                                      range_event);
+                                      range_event, g_last);
         else
             verify_output_tile<D>(p, o, c1, c2, p.eps2 * eps_mult, head, qt, n, row, rs, res, bo);
         if (isfinite(res)) fam_out = res;

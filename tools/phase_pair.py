@@ -69,3 +69,7 @@ for g in range(64):
     print(f"  g={g}: fin wait {t[g, 32] - r}..{t[g, 33] - r}  o_final {t[g, 34] - r}  O read+o_free {t[g, 35] - r}"
           f"  range {t[g, 36] - r}  norm {t[g, 40] - r}  verify {t[g, 37] - r}  store {t[g, 38] - r}  flush {t[g, 39] - r}"
           f"  | next own block S ready {t[g + 2, 1] - r if g + 2 < 64 else -1}")
+    if t[g, 44]:
+        print(f"        per-warp O read {[int(t[g, 52 + w] - r) for w in range(4)]}  range {[int(t[g, 56 + w] - r) for w in range(4)]}")
+        print(f"        sums {t[g, 41] - r}  per-warp norm done {[int(t[g, 48 + w] - r) for w in range(4)]}"
+              f"  per-warp at the check barrier {[int(t[g, 44 + w] - r) for w in range(4)]}")
