@@ -1,6 +1,6 @@
 # round-end style validation: GPU suite, smoke, both bench arms
-mkdir -p gpurun_out/s3g
-python -m pytest tests -m gpu -x -q > gpurun_out/s3g/gputest.log 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s3g/smoke.log 2>&1
-python bench.py > gpurun_out/s3g/bench.json 2> gpurun_out/s3g/bench.err
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/s3g/bench_ref.json 2> gpurun_out/s3g/bench_ref.err
+mkdir -p gpurun_out/s3l
+python -m pytest tests -m gpu -x -q > gpurun_out/s3l/gputest.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s3l/smoke.log 2>&1
+python bench.py > gpurun_out/s3l/bench.json 2> gpurun_out/s3l/bench.err
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/s3l/bench_ref.json 2> gpurun_out/s3l/bench_ref.err
