@@ -41,7 +41,9 @@ struct PairLayout {
     static constexpr int VROWS = PROT ? D + 32 : D;      // rows of the V^T (+VC^T) operand = O columns
     static constexpr int HN_V = VROWS / 2;               // B rows per CTA, P.V
     // 4-stage K / V rings, 3 where the double-buffered Q would not fit (protected d=128)
-    static constexpr int KS = (D == 128 && PROT) ? 3 : 4, VS = KS;
+    // unprotected d=64: 6 stages (A/B: +2-3% at S=2048 / 512; the protected d=64 kernel is row-bound
+    // and measured -0.3% / +-0 with 6, profiles/r02/s3/ab_ring_d64.log)
+    static constexpr int KS = (D == 128 && PROT) ? 3 : ((D == 64 && !PROT) ? 6 : 4), VS = KS;
     static constexpr uint32_t Q_BYTES = NSUB * 16384;  // one Q buffer (two: the next tile's Q loads early)
     static constexpr uint32_t K_CHUNK = HN_S * 128;      // one 64-column chunk of the K half
     static constexpr uint32_t K_STAGE = NSUB * K_CHUNK;
